@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""bench.py -- BASELINE.json metric: MC rollouts/s at 1e8 samples (1/2/4/8 GPU),
+plus p50/p99 latency of the real-time 25k-sample decision batch.
+
+One JSON line on rank 0.  Arms:
+  (default)          the B200 engine (libbrakemc_b200.so through its C-ABI)
+  --impl reference   the reference's own CPU executor (run_parallel, all host
+                     threads) from oracle/_ref, on a bounded prefix sample of
+                     the same workload; rank 0 only.
+
+A step = one pass of the hot path over the batch: predict/bin + RK4 rollout
+of every sample on the rank's shard + the outcome statistics (exceedance
+counts over the TTC-threshold grid, horizon count, extrema, moments, median,
+histogram), then the NCCL allreduce of the count vectors when N > 1.
+`value`: inputs resident in HBM (32 B/sample terms, 3.2 GB at 1e8 >> 126 MB
+L2, so no flush is needed), device-timed with CUDA events on the engine's
+stream, max over ranks.  `e2e`: the same rollouts through bmc_cuda_run (the
+run_cuda core) from pageable host samples to host results, H2D/D2H inside.
+Sample generation is excluded from both (backends.hpp:22-24), and reported.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALGO_FLOPS_PER_STEP = 57   # reference formulation, per RK4 step
+EXEC_FLOPS_PER_STEP = 32   # this kernel (actuator table + exact-doubling FMA)
+SPEC_FP64_OPS = 148 * 64 * 1.965e9  # nominal DADD/DMUL rate at max clock
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--samples", type=float, default=1e8)
+    p.add_argument("--seed", type=int, default=3)
+    p.add_argument("--latency-reps", type=int, default=300)
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--skip-e2e", action="store_true")
+    p.add_argument("--skip-latency", action="store_true")
+    p.add_argument("--skip-cpu", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=5)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[3:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- reference
+
+def reference_arm(args, rank):
+    if rank != 0:
+        return
+    from oracle.pyoracle import Model, Reference, World
+    ref = Reference()
+    cores = ref.hardware_concurrency()
+    model = Model(seed=args.seed)
+    probe, _ = ref.draw_batch(model, 2000)
+    _, t_probe, _ = ref.run(probe, World(), "parallel", 0)
+    per_sample = t_probe / 2000.0
+    budget = max(1.0, 150.0 / max(1, args.steps + args.warmup))  # whole run within minutes
+    n = int(min(args.samples, max(2000, budget / per_sample)))
+    samples, _ = ref.draw_batch(model, n)
+    for _ in range(args.warmup):
+        ref.run(samples[: max(2000, n // 10)], World(), "parallel", 0)
+    times = []
+    for _ in range(args.steps):
+        _, wall, wc = ref.run(samples, World(), "parallel", 0)
+        times.append(wall)
+    value = args.steps * n / sum(times)
+    line = {
+        "impl": "reference", "metric": "MC rollouts/s at 1e8 samples (1/2/4/8 GPU)",
+        "value": value, "unit": "rollouts/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference draw_batch, default UncertaintyModel)",
+        "config": {"workload": "C5 default model seed %d; bounded prefix sample of the 1e8 batch"
+                   % args.seed, "samples_per_step": n, "executor": "run_parallel",
+                   "worker_count": wc, "chunk_size": 256},
+        "cpu_baseline": {"value": value, "unit": "rollouts/s", "cores": cores, "kind": "reference",
+                         "sample": f"{n} samples (prefix of seed {args.seed}), run_parallel"},
+        "e2e": {"value": value, "unit": "rollouts/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, n_total):
+    from oracle.pyoracle import Model, Reference, World
+    ref = Reference()
+    model = Model(seed=args.seed)
+    probe, _ = ref.draw_batch(model, 2000)
+    _, t_probe, _ = ref.run(probe, World(), "parallel", 0)
+    n = int(min(n_total, max(2000, args.cpu_seconds * 2000.0 / t_probe)))
+    samples, _ = ref.draw_batch(model, n)
+    _, wall, wc = ref.run(samples, World(), "parallel", 0)
+    return {"value": n / wall, "unit": "rollouts/s", "cores": wc, "kind": "reference",
+            "sample": f"{n} samples (prefix of the seed-{args.seed} batch), reference "
+                      f"run_parallel with {wc} threads, {wall:.1f} s"}
+
+
+# -------------------------------------------------------------------- b200
+
+def b200_arm(args, rank, world, local_rank, dist):
+    import torch
+    import paper_2604_27193_b200 as bmc
+
+    torch.cuda.set_device(local_rank)
+    n_total = int(args.samples)
+    begin = n_total * rank // world
+    end = n_total * (rank + 1) // world
+    n = end - begin
+    model = bmc.UncertaintyModel(seed=args.seed)
+    sw = bmc.SimWorld()
+
+    t0 = time.perf_counter()
+    samples, clamps = bmc.draw_batch(model, n, first=begin)
+    sample_s = time.perf_counter() - t0
+    terms = bmc.stage_terms(samples, sw)
+    dev_terms = [torch.from_numpy(terms[i]).to(f"cuda:{local_rank}") for i in range(4)]
+    del terms
+    d = torch.empty(n, dtype=torch.float64, device=f"cuda:{local_rank}")
+    st = torch.empty(n, dtype=torch.int32, device=f"cuda:{local_rank}")
+    hz = torch.empty(n, dtype=torch.uint8, device=f"cuda:{local_rank}")
+    total_steps = torch.zeros(1, dtype=torch.int64, device=f"cuda:{local_rank}")
+
+    ex = bmc.CudaExecutor(local_rank)
+    peak_ops, _ = ex.fp64_peak(reps=5)
+    stream = torch.cuda.ExternalStream(ex.stream_handle, device=f"cuda:{local_rank}")
+
+    # C4-style TTC threshold sweep: T in {1.0, 1.25, ..., 6.0} s, closing 30 m/s
+    ttc = [1.0 + 0.25 * k for k in range(21)]
+    headways = [t * model.initial_speed[0] for t in ttc]
+    launches = [0]
+    kernel_ms = []
+
+    def step(record=False):
+        total_steps.zero_()
+        ex.rollout_device(dev_terms, (d, st, hz), sw, total_steps=total_steps)
+        nl = ex.last_launches()
+        counts = ex.exceedance_counts(d, hz, headways)
+        nl += ex.last_launches()
+        if record:
+            kernel_ms.append(ex.last_kernel_ms()[0])
+        summ = ex.summarize(d, hz, 2.0)
+        nl += ex.last_launches()
+        vec = torch.tensor(list(counts) + [summ["horizon_count"]], dtype=torch.int64,
+                           device=f"cuda:{local_rank}")
+        if world > 1:
+            dist.all_reduce(vec)
+        launches[0] += nl if record else 0
+        return vec, summ
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    steps_sum = 0
+    for _ in range(args.steps):
+        vec, summ = step(record=True)
+        steps_sum += int(total_steps.item())
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=f"cuda:{local_rank}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    value = n_total / (ms_per_step * 1e-3)
+
+    roll_ms = sum(kernel_ms) / len(kernel_ms)
+    steps_per_launch = steps_sum / args.steps
+    achieved = ALGO_FLOPS_PER_STEP * steps_per_launch / (roll_ms * 1e-3)
+    executed = EXEC_FLOPS_PER_STEP * steps_per_launch / (roll_ms * 1e-3)
+
+    # ---- e2e through the run_cuda core (host samples -> host results)
+    e2e = None
+    if not args.skip_e2e:
+        out = np.empty(n, dtype=bmc.RESULT_DTYPE)
+        for _ in range(max(1, args.warmup // 2)):
+            ex.run(samples, sw, out=out)
+        if world > 1:
+            dist.barrier()
+        tt = time.perf_counter()
+        reps = max(1, min(args.steps, 3))
+        for _ in range(reps):
+            rep = ex.run(samples, sw, out=out)
+        e2e_s = (time.perf_counter() - tt) / reps
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local_rank}")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_total / float(te.item()), "unit": "rollouts/s",
+               "h2d_bytes_per_step": rep.h2d_bytes, "d2h_bytes_per_step": rep.d2h_bytes,
+               "path": "bmc_cuda_run (run_cuda core): pageable AoS samples -> terms staging "
+                       "(host pool) -> pinned -> H2D -> bin+rollout -> D2H -> AoS results",
+               "reps": reps}
+        del out
+
+    # ---- real-time decision batch (C2): 25k samples, p50/p99 over replays
+    latency = None
+    if rank == 0 and not args.skip_latency:
+        lat_samples = [bmc.draw_batch(bmc.UncertaintyModel(seed=s), 25000)[0] for s in range(1, 9)]
+        out = np.empty(25000, dtype=bmc.RESULT_DTYPE)
+        for s in lat_samples:
+            ex.run(s, sw, out=out)
+        sim_ms, full_ms = [], []
+        for k in range(args.latency_reps):
+            s = lat_samples[k % len(lat_samples)]
+            t1 = time.perf_counter()
+            ex.run(s, sw, out=out)
+            sim_ms.append(1e3 * (time.perf_counter() - t1))
+        for k in range(min(100, args.latency_reps)):
+            t1 = time.perf_counter()
+            s, _ = bmc.draw_batch(bmc.UncertaintyModel(seed=1000 + k), 25000)
+            ex.run(s, sw, out=out)
+            full_ms.append(1e3 * (time.perf_counter() - t1))
+        q = lambda v, p: float(np.percentile(np.array(v), p))
+        latency = {"samples": 25000, "budget_ms": 530.0,
+                   "sim_only_ms": {"p50": q(sim_ms, 50), "p99": q(sim_ms, 99),
+                                   "reps": len(sim_ms)},
+                   "with_sampling_ms": {"p50": q(full_ms, 50), "p99": q(full_ms, 99),
+                                        "reps": len(full_ms)},
+                   "path": "bmc_cuda_run host->host (H2D, bin, rollout, D2H)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        cpu = cpu_baseline(args, n_total)
+
+    if rank == 0:
+        line = {
+            "metric": "MC rollouts/s at 1e8 samples (1/2/4/8 GPU)",
+            "value": value, "unit": "rollouts/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (host draw_batch, default UncertaintyModel, bit-identical to "
+                    "the reference sampler)",
+            "config": {"workload": "C5: %d default-model samples (seed %d), contiguous index "
+                                   "shards per GPU; per step: bin + RK4 rollout + exceedance "
+                                   "counts (21 TTC thresholds) + summarize + allreduce"
+                                   % (n_total, args.seed),
+                       "samples": n_total, "dt": sw.dt, "t_max": sw.t_max,
+                       "parallelism": f"shard{world}",
+                       "l2": "no flush: inputs 32 B/sample = %.2f GB per GPU >> 126 MB L2"
+                             % (32 * n / 1e9),
+                       "sampling_s": sample_s, "clamp_count": clamps},
+            "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
+                         "unit": "TFLOP/s", "frac": achieved / peak_ops, "traffic": None,
+                         "kernel": "rollout_kernel", "kernel_ms": roll_ms,
+                         "rk4_steps_per_launch": steps_per_launch,
+                         "algorithmic_flops_per_step": ALGO_FLOPS_PER_STEP,
+                         "executed_flops_per_step": EXEC_FLOPS_PER_STEP,
+                         "executed_frac": executed / peak_ops,
+                         "peak_source": "measured in-run: unfused DADD/DMUL probe "
+                                        "(MEASURED_PEAKS.json has no FP64 entry)",
+                         "spec_peak_tflops": SPEC_FP64_OPS / 1e12},
+            "e2e": e2e,
+            "latency_25k": latency,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": launches[0],
+        }
+        print(json.dumps(line), flush=True)
+    ex.close()
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    try:
+        b200_arm(args, rank, world, local_rank, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

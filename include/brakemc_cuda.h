@@ -1,0 +1,201 @@
+/*
+ * brakemc_cuda.h -- C-ABI of the B200 (sm_100a) Monte Carlo rollout engine.
+ *
+ * This is the drop-in boundary for the reference's executor family
+ * (/root/reference/proj/include/brakemc/backends.hpp:18-45).  The reference
+ * has no FFI; its extension point is "an actual GPU backend ... behind the
+ * same executor interface".  The C++ executor
+ * brakemc::run_cuda (include/brakemc/cuda_executor.hpp) is a thin adapter
+ * over these entry points; Python tests/bench bind them through ctypes.
+ *
+ * Conventions
+ *   - Plain C types only; no exceptions cross this boundary.
+ *   - Every int-returning call returns BMC_OK (0) or a negative BMC_E_* code;
+ *     the message is available from bmc_last_error() (thread-local) and,
+ *     for context calls, bmc_cuda_last_error(ctx).
+ *   - BMC_E_CONFIG mirrors brakemc::ConfigError (errors.hpp:10-20): the
+ *     message starts with the offending field path, e.g.
+ *     "batch: must be non-empty" (backends.cpp:41-43).
+ *   - Struct layouts equal the reference value types byte for byte
+ *     (static_assert'ed in cuda_executor.cpp), so a std::vector<RolloutResult>
+ *     or std::vector<ScenarioSample> can be passed by .data().
+ *   - There is NO CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with BMC_E_CUDA.
+ */
+#ifndef BRAKEMC_CUDA_H
+#define BRAKEMC_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BMC_ABI_VERSION 1
+
+enum {
+    BMC_OK = 0,
+    BMC_E_CONFIG = -1,  /* invalid argument (ConfigError analogue)        */
+    BMC_E_DOMAIN = -2,  /* friction_limit denominator <= 0 (domain_error) */
+    BMC_E_CUDA = -3,    /* CUDA runtime / launch failure                  */
+    BMC_E_NOMEM = -4,   /* host or device allocation failed               */
+    BMC_E_RANGE = -5    /* capacity exceeded (e.g. histogram buffer)      */
+};
+
+/* == brakemc::ScenarioSample (dynamics.hpp:36-44), 40 bytes */
+typedef struct {
+    double initial_speed, friction, grade, mass, drag_coeff;
+} bmc_sample;
+
+/* == brakemc::RolloutResult (integrator.hpp:14-19), 32 bytes */
+typedef struct {
+    double stop_distance;
+    double stop_time;
+    int64_t steps;
+    uint8_t hit_horizon;
+    uint8_t pad_[7];
+} bmc_result;
+
+/* SimConfig (dynamics.hpp:54-60) + VehicleGeometry (:27-33) +
+ * PhysicalConstants (:17-24), flattened in that order. */
+typedef struct {
+    double dt, t_max, brake_cmd;
+    double cg_height, wheelbase, actuator_tau;
+    double gravity, air_density, frontal_area;
+} bmc_world;
+
+/* == brakemc::NormalSpec (sampling.hpp:17-20) */
+typedef struct {
+    double mean, sd;
+} bmc_normal;
+
+/* == brakemc::UncertaintyModel (sampling.hpp:24-33), 88 bytes */
+typedef struct {
+    uint64_t seed;
+    bmc_normal initial_speed, friction, grade, mass, drag_coeff;
+} bmc_model;
+
+/* Per-sample rollout inputs staged SoA: the sample-varying part of
+ * brakemc::RolloutTerms (dynamics.hpp:96-106) plus v0.  brake_cmd and
+ * inv_tau are batch constants and travel in bmc_world. 32 B/sample. */
+typedef struct {
+    const double* initial_speed;
+    const double* brake_floor;
+    const double* drag_factor;
+    const double* grade_accel;
+} bmc_terms;
+
+/* Compact per-sample outputs (13 B/sample).  Any pointer may be NULL
+ * (stats-only mode).  stop_time is not stored: it is (double)steps * dt. */
+typedef struct {
+    double* stop_distance;
+    int32_t* steps;
+    uint8_t* hit_horizon;
+} bmc_outputs;
+
+/* Scheduling knobs; zero-initialised means "defaults". Results never
+ * depend on these (only timing does), exactly like run_parallel's chunk
+ * size (backends.hpp:36-41). */
+typedef struct {
+    int32_t schedule;       /* 0 = default (binned), 1 = index order, 2 = binned by predicted stop step */
+    int32_t block_threads;  /* 0 = default */
+    int32_t table_mode;     /* 0 = auto, 1 = shared-mem a-table, 2 = global a-table, 3 = no table */
+    int32_t host_threads;   /* 0 = all hardware threads (host staging / unpack) */
+    uint64_t chunk_samples; /* 0 = default pipeline chunk for bmc_cuda_run */
+} bmc_run_opts;
+
+/* Timing breakdown of one bmc_cuda_run call (seconds). */
+typedef struct {
+    double wall_s;        /* whole call: staging + H2D + kernels + D2H + unpack */
+    double kernel_ms;     /* sum of rollout-kernel event times */
+    double predict_ms;    /* sum of predictor + binning kernel event times */
+    uint64_t total_steps; /* sum of executed RK4 steps (roofline numerator) */
+    uint64_t h2d_bytes, d2h_bytes;
+    uint32_t launches;    /* kernels this call launched */
+    uint32_t chunks;
+} bmc_run_info;
+
+typedef struct bmc_ctx bmc_ctx;
+
+/* ------------------------------------------------------------- context */
+int bmc_abi_version(void);
+const char* bmc_last_error(void);
+int bmc_device_count(int* out);
+int bmc_cuda_init(int device, bmc_ctx** out);
+void bmc_cuda_destroy(bmc_ctx* ctx);
+const char* bmc_cuda_last_error(const bmc_ctx* ctx);
+int bmc_cuda_sync(bmc_ctx* ctx);
+/* the context's compute stream (cudaStream_t) */
+void* bmc_cuda_stream(bmc_ctx* ctx);
+
+/* ------------------------------------------------ host-side producers */
+/* draw_batch (sampling.cpp:67-100) restricted to sample indices
+ * [first, first + n); bit-identical to the same slice of draw_batch(model, N)
+ * because the stream is counter-based (sampling.hpp:3-6). threads <= 0: all. */
+int bmc_draw_range(const bmc_model* model, uint64_t first, size_t n, bmc_sample* out,
+                   uint64_t* clamp_count, int threads);
+/* RolloutTerms::from (dynamics.cpp:57-68) for each sample, SoA out. */
+int bmc_stage_terms(const bmc_sample* samples, size_t n, const bmc_world* world,
+                    double* initial_speed, double* brake_floor, double* drag_factor,
+                    double* grade_accel, int threads);
+
+/* ------------------------------------------------------------ executor */
+/* Drop-in core of brakemc::run_cuda: host AoS samples in, host AoS results
+ * out (index-aligned, bit-identical to run_sequential).  Synchronous.
+ * Host staging, H2D, kernels, D2H and unpack are pipelined in chunks. */
+int bmc_cuda_run(bmc_ctx* ctx, const bmc_sample* samples, size_t n, const bmc_world* world,
+                 const bmc_run_opts* opts, bmc_result* out, bmc_run_info* info);
+
+/* Device-resident rollout: terms and outputs are device pointers; enqueued
+ * on `stream` (NULL = the context's stream); returns without synchronising.
+ * total_steps_dev (device uint64, nullable) accumulates executed steps. */
+int bmc_cuda_rollout_device(bmc_ctx* ctx, const bmc_terms* terms, size_t n,
+                            const bmc_world* world, const bmc_run_opts* opts,
+                            const bmc_outputs* out, unsigned long long* total_steps_dev,
+                            void* stream);
+
+/* Last rollout kernel's device time in ms, via CUDA events recorded around
+ * it on its own stream (valid after the stream is synchronised). */
+int bmc_cuda_last_kernel_ms(bmc_ctx* ctx, float* rollout_ms, float* predict_ms);
+/* Number of kernels the last device call enqueued. */
+int bmc_cuda_last_launches(bmc_ctx* ctx, uint32_t* launches);
+
+/* ---------------------------------------------------------- statistics */
+/* Everything analysis.cpp derives from a result vector, computed on device
+ * from the compact outputs.  Counts / extrema / histogram / order statistics
+ * are exact; mean/sd/skewness use an order-independent compensated sum
+ * (the reference sums sequentially, analysis.cpp:34-37). */
+typedef struct {
+    uint64_t n, horizon_count, bins;
+    double mean, sd, min, max, median, skewness, origin, bin_width;
+    int32_t right_skewed;
+    int32_t pad_;
+} bmc_summary;
+
+/* summarize (analysis.cpp:13-76). hist: host buffer of hist_cap counts
+ * (nullable); BMC_E_RANGE if hist_cap < bins. */
+int bmc_cuda_summarize(bmc_ctx* ctx, const double* stop_distance, const uint8_t* hit_horizon,
+                       size_t n, double bin_width, bmc_summary* out, uint64_t* hist,
+                       size_t hist_cap);
+/* numerators of collision_probability (analysis.cpp:145-159) for m headways
+ * (any order): counts[j] = #{hit_horizon || d > headways[j]}. */
+int bmc_cuda_exceedance(bmc_ctx* ctx, const double* stop_distance, const uint8_t* hit_horizon,
+                        size_t n, const double* headways, size_t m, uint64_t* counts);
+/* Exact order statistics: out[j] = ranks[j]-th smallest (1-based) value of
+ * stop_distance, over non-horizon results only when exclude_horizon != 0.
+ * Ranks outside [1, count] give NaN. */
+int bmc_cuda_order_stats(bmc_ctx* ctx, const double* stop_distance, const uint8_t* hit_horizon,
+                         size_t n, int exclude_horizon, const uint64_t* ranks, size_t m,
+                         double* out, uint64_t* count_out);
+
+/* ------------------------------------------------------- measurement */
+/* FP64 DADD/DMUL issue-rate probe (the rollout's roofline denominator;
+ * MEASURED_PEAKS.json carries no FP64 entry).  Independent chains of
+ * unfused add/mul at full occupancy; best of `reps` launches, CUDA events. */
+int bmc_cuda_fp64_peak(bmc_ctx* ctx, int reps, double* ops_per_s, double* best_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,387 @@
+// bmc_kernels.cu -- sm_100a kernels of the Monte Carlo rollout path.
+//
+// Compiled with nvcc -gencode arch=compute_100a,code=sm_100a -fmad=false.
+// Every FP64 operation of the rollout is spelled with an explicit _rn
+// intrinsic, so the association order is the reference's
+// (integrator.hpp:39-68, dynamics.hpp:115-132; paths under
+// /root/reference/proj) regardless of compiler flags.
+//
+// Bound: the FP64 DADD/DMUL pipe.  Per RK4 step the
+// reference formulation executes 57 FP64 flops; this kernel executes 32:
+//   * the actuator lane (a, s2.a, s3.a, s4.a) is sample-independent and is
+//     read from a per-batch table (bmc_host.cpp build_actuator_table): -21
+//     (+ the table reaches an exact fixed point, after which the per-lane
+//     clamped brake values are loop constants);
+//   * k1 + 2.0*k2 is computed as fma(2.0, k2, k1): 2.0*k2 is exact in
+//     binary64, so the single rounding of the FMA equals the reference's
+//     rounding of the add, bit for bit (also for signed zeros): -4.
+// Divergence from mixed stop times is removed by binning samples on a cheap
+// FP32 prediction of their stop step (predict_kernel + counting sort), so a
+// warp's 32 lanes retire within a few steps of each other; warps pull
+// 32-sample groups longest-first from a global counter (persistent CTAs).
+#include "bmc_kernels.h"
+
+#include <cub/block/block_scan.cuh>
+
+namespace bmc {
+namespace {
+
+int sm_count_cached(int device);
+
+__device__ __forceinline__ double clamp_brake(double a, double floor_) {
+    // dynamics.hpp:82-84 (ternary semantics, not fmax)
+    return a > floor_ ? a : floor_;
+}
+
+// longitudinal_accel (dynamics.hpp:115-118): (braking - D*(v*v)) - G
+__device__ __forceinline__ double accel(double braking, double v, double D, double G) {
+    return __dsub_rn(__dsub_rn(braking, __dmul_rn(D, __dmul_rn(v, v))), G);
+}
+
+// The (position, speed) lanes of rk4_step (integrator.hpp:39-68) for given
+// clamped stage brake values b1..b4.  k_i.d_position = stage speed, so the
+// position stages (dead code in the reference) are not formed.
+__device__ __forceinline__ void rk4_xv(double& x, double& v, double b1, double b2, double b3,
+                                       double b4, double D, double G, double dt, double half,
+                                       double sixth) {
+    const double k1 = accel(b1, v, D, G);
+    const double s2 = __dadd_rn(v, __dmul_rn(half, k1));
+    const double k2 = accel(b2, s2, D, G);
+    const double s3 = __dadd_rn(v, __dmul_rn(half, k2));
+    const double k3 = accel(b3, s3, D, G);
+    const double s4 = __dadd_rn(v, __dmul_rn(dt, k3));
+    const double k4 = accel(b4, s4, D, G);
+    // ((k1 + 2k2) + 2k3) + k4 with exact doubling folded into FMAs
+    const double cv = __dadd_rn(__fma_rn(2.0, k3, __fma_rn(2.0, k2, k1)), k4);
+    const double cx = __dadd_rn(__fma_rn(2.0, s3, __fma_rn(2.0, s2, v)), s4);
+    x = __dadd_rn(x, __dmul_rn(sixth, cx));
+    v = __dadd_rn(v, __dmul_rn(sixth, cv));
+}
+
+// Actuator lane of rk4_step for the no-table fallback (dynamics.hpp:130).
+__device__ __forceinline__ StageA actuator_stages(double a, double cmd, double inv_tau,
+                                                  double dt, double half, double sixth,
+                                                  double* a_next) {
+    const double k1 = __dmul_rn(__dsub_rn(cmd, a), inv_tau);
+    const double s2 = __dadd_rn(a, __dmul_rn(half, k1));
+    const double k2 = __dmul_rn(__dsub_rn(cmd, s2), inv_tau);
+    const double s3 = __dadd_rn(a, __dmul_rn(half, k2));
+    const double k3 = __dmul_rn(__dsub_rn(cmd, s3), inv_tau);
+    const double s4 = __dadd_rn(a, __dmul_rn(dt, k3));
+    const double k4 = __dmul_rn(__dsub_rn(cmd, s4), inv_tau);
+    const double c = __dadd_rn(__fma_rn(2.0, k3, __fma_rn(2.0, k2, k1)), k4);
+    *a_next = __dadd_rn(a, __dmul_rn(sixth, c));
+    return StageA{a, s2, s3, s4};
+}
+
+template <int MODE>
+__device__ __forceinline__ StageA load_stage(const StageA* tab, int n) {
+    if (MODE == kTableGlobal) {
+        const double2* p = reinterpret_cast<const double2*>(tab) + 2 * n;
+        const double2 lo = __ldg(p), hi = __ldg(p + 1);
+        return StageA{lo.x, lo.y, hi.x, hi.y};
+    } else {
+        const double2* p = reinterpret_cast<const double2*>(tab) + 2 * n;
+        const double2 lo = p[0], hi = p[1];
+        return StageA{lo.x, lo.y, hi.x, hi.y};
+    }
+}
+
+// simulate_rollout (integrator.cpp:13-29) for sample j.
+template <int MODE>
+__device__ __forceinline__ int32_t run_one(const RolloutArgs& A, const StageA* tab, int len,
+                                           uint64_t j) {
+    const double D = A.drag[j];
+    const double G = A.grade[j];
+    const double F = A.brake_floor[j];
+    double v = A.v0[j];
+    double x = 0.0;
+    const int32_t M = A.max_steps;
+    int32_t n = 0;
+    bool stopped = false;
+    if (MODE == kTableNone) {
+        double a = 0.0;
+        for (; n < M; ++n) {
+            double an;
+            const StageA s = actuator_stages(a, A.brake_cmd, A.inv_tau, A.dt, A.half, A.sixth, &an);
+            rk4_xv(x, v, clamp_brake(s.a0, F), clamp_brake(s.a1, F), clamp_brake(s.a2, F),
+                   clamp_brake(s.a3, F), D, G, A.dt, A.half, A.sixth);
+            a = an;
+            if (v <= 0.0) {
+                stopped = true;
+                break;
+            }
+        }
+    } else {
+        const int32_t head = min(len - 1, M);
+        for (; n < head; ++n) {
+            const StageA s = load_stage<MODE>(tab, n);
+            rk4_xv(x, v, clamp_brake(s.a0, F), clamp_brake(s.a1, F), clamp_brake(s.a2, F),
+                   clamp_brake(s.a3, F), D, G, A.dt, A.half, A.sixth);
+            if (v <= 0.0) {
+                stopped = true;
+                break;
+            }
+        }
+        if (!stopped && n < M) {
+            // Past the actuator fixed point every stage value is constant,
+            // hence so are the clamped brake values of this lane.
+            const StageA s = load_stage<MODE>(tab, len - 1);
+            const double b1 = clamp_brake(s.a0, F), b2 = clamp_brake(s.a1, F);
+            const double b3 = clamp_brake(s.a2, F), b4 = clamp_brake(s.a3, F);
+            for (; n < M; ++n) {
+                rk4_xv(x, v, b1, b2, b3, b4, D, G, A.dt, A.half, A.sixth);
+                if (v <= 0.0) {
+                    stopped = true;
+                    break;
+                }
+            }
+        }
+    }
+    const int32_t steps = stopped ? n + 1 : M;
+    if (A.stop_distance) A.stop_distance[j] = x;
+    if (A.steps) A.steps[j] = steps;
+    if (A.hit_horizon) A.hit_horizon[j] = stopped ? 0 : 1;
+    return steps;
+}
+
+template <int MODE, int BT>
+__global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const StageA* tab = A.table;
+    const int len = A.table_len;
+    if (MODE == kTableShared) {
+        const double2* src = reinterpret_cast<const double2*>(A.table);
+        double2* dst = reinterpret_cast<double2*>(smem_raw);
+        for (int i = threadIdx.x; i < 2 * len; i += BT) dst[i] = src[i];
+        __syncthreads();
+        tab = reinterpret_cast<const StageA*>(smem_raw);
+    }
+    const unsigned lane = threadIdx.x & 31u;
+    unsigned long long my_steps = 0;
+    for (;;) {
+        unsigned g = 0;
+        if (lane == 0) g = atomicAdd(A.work_counter, 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        const uint64_t base = static_cast<uint64_t>(g) * 32u;
+        if (base >= A.n) break;
+        const uint64_t i = base + lane;
+        if (i < A.n) {
+            const uint64_t j = A.perm ? static_cast<uint64_t>(A.perm[i]) : i;
+            my_steps += static_cast<unsigned long long>(max(run_one<MODE>(A, tab, len, j), 0));
+        }
+    }
+    if (A.total_steps) {
+        for (int o = 16; o > 0; o >>= 1) my_steps += __shfl_down_sync(0xffffffffu, my_steps, o);
+        if (lane == 0 && my_steps) atomicAdd(A.total_steps, my_steps);
+    }
+}
+
+// ---------------------------------------------------------------- binning
+
+constexpr int kMaxBuckets = 4096;
+
+// FP32 coarse-step RK4 of the speed lane (brake_accel sampled from the exact
+// actuator table) -> predicted stop step -> bucket (descending).  Only the
+// schedule depends on this; results never do.
+__global__ void __launch_bounds__(256) predict_kernel(const PredictArgs P) {
+    extern __shared__ float s_a[];
+    __shared__ unsigned int s_hist[kMaxBuckets];
+    for (int i = threadIdx.x; i < P.coarse_len; i += blockDim.x) s_a[i] = P.coarse_a[i];
+    for (int i = threadIdx.x; i < P.buckets; i += blockDim.x) s_hist[i] = 0u;
+    __syncthreads();
+    const float h = P.h, hh = 0.5f * P.h, h6 = P.h / 6.0f;
+    const int last = P.coarse_len - 1;
+    const int kmax = (P.coarse_len - 1) / 2;  // coarse steps to the horizon
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P.n;
+         i += stride) {
+        float v = static_cast<float>(P.v0[i]);
+        const float F = static_cast<float>(P.brake_floor[i]);
+        const float D = static_cast<float>(P.drag[i]);
+        const float G = static_cast<float>(P.grade[i]);
+        int pred = P.max_steps;
+        for (int k = 0; k < kmax; ++k) {
+            const float b1 = fmaxf(s_a[min(2 * k, last)], F);
+            const float b2 = fmaxf(s_a[min(2 * k + 1, last)], F);
+            const float b4 = fmaxf(s_a[min(2 * k + 2, last)], F);
+            const float k1 = b1 - D * v * v - G;
+            const float v2 = v + hh * k1;
+            const float k2 = b2 - D * v2 * v2 - G;
+            const float v3 = v + hh * k2;
+            const float k3 = b2 - D * v3 * v3 - G;
+            const float v4 = v + h * k3;
+            const float k4 = b4 - D * v4 * v4 - G;
+            const float vn = v + h6 * (k1 + 2.0f * k2 + 2.0f * k3 + k4);
+            if (vn <= 0.0f) {
+                const float frac = v / (v - vn);
+                const float tstar = (static_cast<float>(k) + frac) * h;
+                pred = static_cast<int>(ceilf(tstar * P.inv_dt));
+                break;
+            }
+            v = vn;
+        }
+        pred = max(1, min(pred, P.max_steps));
+        const int bucket = min((P.max_steps - pred) / P.bucket_width, P.buckets - 1);
+        P.keys[i] = static_cast<uint16_t>(bucket);
+        atomicAdd(&s_hist[bucket], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < P.buckets; b += blockDim.x) {
+        const unsigned int c = s_hist[b];
+        if (c) atomicAdd(&P.hist[b], c);
+    }
+}
+
+__global__ void __launch_bounds__(1024) bin_scan_kernel(unsigned int* hist, int buckets) {
+    // exclusive scan, in place: counts -> start cursor of each bucket
+    using Scan = cub::BlockScan<unsigned int, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    constexpr int kPer = kMaxBuckets / 1024;
+    unsigned int items[kPer];
+    for (int k = 0; k < kPer; ++k) {
+        const int b = threadIdx.x * kPer + k;
+        items[k] = b < buckets ? hist[b] : 0u;
+    }
+    Scan(tmp).ExclusiveSum(items, items);
+    for (int k = 0; k < kPer; ++k) {
+        const int b = threadIdx.x * kPer + k;
+        if (b < buckets) hist[b] = items[k];
+    }
+}
+
+__global__ void __launch_bounds__(256) bin_scatter_kernel(const uint16_t* keys, uint64_t n,
+                                                          unsigned int* cursor, uint32_t* perm) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const unsigned lane = threadIdx.x & 31u;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < n;
+         base += stride) {
+        const uint64_t i = base + threadIdx.x;
+        const bool valid = i < n;
+        const unsigned active = __ballot_sync(0xffffffffu, valid);
+        if (!valid) continue;
+        const unsigned key = keys[i];
+        const unsigned peers = __match_any_sync(active, key);
+        const int leader = __ffs(peers) - 1;
+        const unsigned rank = __popc(peers & ((1u << lane) - 1u));
+        unsigned int start = 0;
+        if (static_cast<int>(lane) == leader) start = atomicAdd(&cursor[key], __popc(peers));
+        start = __shfl_sync(peers, start, leader);
+        perm[start + rank] = static_cast<uint32_t>(i);
+    }
+}
+
+// FP64 issue-rate probe: 8 independent chains per thread of unfused
+// x = x*a + b (one DMUL + one DADD each), so the pipe, not latency, binds.
+__global__ void __launch_bounds__(512) fp64_probe_kernel(double* out, int iters, double a,
+                                                         double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = 1.0 + 1e-9 * (threadIdx.x + 37 * k);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = __dadd_rn(__dmul_rn(x[k], a), b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s = __dadd_rn(s, x[k]);
+    if (s == 12345.678) out[0] = s;  // never true; keeps the chains alive
+}
+
+template <int MODE, int BT>
+cudaError_t launch_rollout_t(const RolloutArgs& a, cudaStream_t s) {
+    size_t smem = 0;
+    if (MODE == kTableShared) {
+        smem = static_cast<size_t>(a.table_len) * sizeof(StageA);
+        const cudaError_t e = cudaFuncSetAttribute(rollout_kernel<MODE, BT>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    int dev = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rollout_kernel<MODE, BT>,
+                                                                  BT, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t groups = (a.n + 31) / 32;
+    const uint64_t need = (groups + BT / 32 - 1) / (BT / 32);
+    const uint64_t resident = static_cast<uint64_t>(per_sm) * static_cast<uint64_t>(sm_count_cached(dev));
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(need, resident)));
+    rollout_kernel<MODE, BT><<<grid, BT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_rollout_m(const RolloutArgs& a, int block_threads, cudaStream_t s) {
+    switch (block_threads) {
+        case 256: return launch_rollout_t<MODE, 256>(a, s);
+        case 512: return launch_rollout_t<MODE, 512>(a, s);
+        case 768: return launch_rollout_t<MODE, 768>(a, s);
+        case 1024: return launch_rollout_t<MODE, 1024>(a, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+int sm_count_cached(int device) {
+    static int cache[64] = {0};
+    if (device < 0 || device >= 64) return sm_count(device);
+    if (cache[device] == 0) cache[device] = sm_count(device);
+    return cache[device];
+}
+
+}  // namespace
+
+int sm_count(int device) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    return v;
+}
+
+cudaError_t launch_rollout(const RolloutArgs& a, int table_mode, int block_threads, cudaStream_t s) {
+    switch (table_mode) {
+        case kTableShared: return launch_rollout_m<kTableShared>(a, block_threads, s);
+        case kTableGlobal: return launch_rollout_m<kTableGlobal>(a, block_threads, s);
+        case kTableNone: return launch_rollout_m<kTableNone>(a, block_threads, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_fp64_probe(double* out, int iters, uint64_t* ops, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int blocks = sm_count(dev) * 4;
+    fp64_probe_kernel<<<blocks, 512, 0, s>>>(out, iters, 0.99999999, 1e-8);
+    *ops = static_cast<uint64_t>(blocks) * 512u * static_cast<uint64_t>(iters) * 16u;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_predict(const PredictArgs& a, cudaStream_t s) {
+    if (a.buckets > kMaxBuckets || a.buckets < 1) return cudaErrorInvalidValue;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t blocks_needed = (a.n + 255) / 256;
+    const int grid = static_cast<int>(std::min<uint64_t>(blocks_needed,
+                                                         static_cast<uint64_t>(sm_count(dev)) * 8));
+    predict_kernel<<<grid, 256, static_cast<size_t>(a.coarse_len) * sizeof(float), s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bin_scan(unsigned int* hist, int buckets, cudaStream_t s) {
+    if (buckets > kMaxBuckets) return cudaErrorInvalidValue;
+    bin_scan_kernel<<<1, 1024, 0, s>>>(hist, buckets);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* cursor,
+                               uint32_t* perm, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t blocks_needed = (n + 255) / 256;
+    const int grid = static_cast<int>(std::min<uint64_t>(blocks_needed,
+                                                         static_cast<uint64_t>(sm_count(dev)) * 8));
+    bin_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, cursor, perm);
+    return cudaGetLastError();
+}
+
+}  // namespace bmc

@@ -1,0 +1,74 @@
+// bmc_kernels.h -- launch interface of the sm_100a kernels (bmc_kernels.cu,
+// bmc_stats.cu).  Host-only callers (bmc_capi.cpp) see plain structs.
+#pragma once
+
+#include "bmc_internal.h"
+
+#include <cuda_runtime.h>
+
+namespace bmc {
+
+enum TableMode : int { kTableAuto = 0, kTableShared = 1, kTableGlobal = 2, kTableNone = 3 };
+enum Schedule : int { kScheduleDefault = 0, kScheduleIndex = 1, kScheduleBinned = 2 };
+
+// Largest actuator table kept in shared memory (entries of 32 B).
+constexpr int kSmemTableMax = 6784;  // 217 KB of the 227 KB opt-in limit
+
+struct RolloutArgs {
+    const double* v0;
+    const double* brake_floor;
+    const double* drag;
+    const double* grade;
+    const uint32_t* perm;  // nullable: index order
+    uint64_t n;
+    double dt, half, sixth, brake_cmd, inv_tau;
+    int32_t max_steps;
+    const StageA* table;   // device, table_len entries (unused for kTableNone)
+    int32_t table_len;
+    double* stop_distance; // nullable
+    int32_t* steps;        // nullable
+    uint8_t* hit_horizon;  // nullable
+    unsigned long long* total_steps;  // nullable
+    unsigned int* work_counter;       // device, zeroed before launch
+};
+
+struct PredictArgs {
+    const double* v0;
+    const double* brake_floor;
+    const double* drag;
+    const double* grade;
+    uint64_t n;
+    const float* coarse_a;  // brake_accel at t = k * h/2, k = 0..coarse_len-1
+    int32_t coarse_len;
+    float h;                // coarse step (s)
+    float inv_dt;
+    int32_t max_steps;
+    int32_t bucket_width;   // steps per bucket
+    int32_t buckets;
+    uint16_t* keys;         // out: bucket per sample (descending predicted steps)
+    unsigned int* hist;     // out: per-bucket counts (zeroed before launch)
+};
+
+struct LaunchShape {
+    int block_threads;
+    int grid;
+    size_t smem;
+};
+
+int sm_count(int device);
+
+// Persistent launch: grid = min(resident CTAs, 32-sample groups / warps per CTA).
+cudaError_t launch_rollout(const RolloutArgs& a, int table_mode, int block_threads, cudaStream_t s);
+cudaError_t launch_predict(const PredictArgs& a, cudaStream_t s);
+cudaError_t launch_fp64_probe(double* out, int iters, uint64_t* ops, cudaStream_t s);
+cudaError_t launch_bin_scan(unsigned int* hist_to_cursor, int buckets, cudaStream_t s);
+cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* cursor,
+                               uint32_t* perm, cudaStream_t s);
+
+// statistics (bmc_stats.cu)
+struct StatsScratch {
+    void* buf = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace bmc

@@ -1,0 +1,299 @@
+"""Python face of the B200 rollout engine (tests, bench and smoke use it).
+
+The product's host side is C/C++ (the reference is a C++ library): the
+executor is ``brakemc::run_cuda`` (include/brakemc/cuda_executor.hpp) over
+the C-ABI in include/brakemc_cuda.h.  This module binds the same C-ABI with
+ctypes and mirrors the reference API names (/root/reference/proj/include/
+brakemc/{sampling,backends,analysis}.hpp) so parity tests read like the
+reference's own tests.  Device buffers are torch tensors (plumbing only).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+SAMPLE_DTYPE = np.dtype(
+    [("initial_speed", "<f8"), ("friction", "<f8"), ("grade", "<f8"), ("mass", "<f8"),
+     ("drag_coeff", "<f8")])
+RESULT_DTYPE = np.dtype(
+    [("stop_distance", "<f8"), ("stop_time", "<f8"), ("steps", "<i8"), ("hit_horizon", "u1"),
+     ("pad_", "V7")])
+
+# schedule / table modes (bmc_run_opts)
+SCHEDULE = {"default": 0, "index": 1, "binned": 2}
+TABLE = {"auto": 0, "shared": 1, "global": 2, "none": 3}
+
+
+@dataclass
+class SimWorld:
+    """SimConfig + VehicleGeometry + PhysicalConstants (dynamics.hpp:17-60)."""
+    dt: float = 0.001
+    t_max: float = 10.0
+    brake_cmd: float = -6.0
+    cg_height: float = 0.5
+    wheelbase: float = 2.7
+    actuator_tau: float = 0.15
+    gravity: float = 9.81
+    air_density: float = 1.225
+    frontal_area: float = 2.2
+
+    def c(self) -> N.World:
+        return N.World(self.dt, self.t_max, self.brake_cmd, self.cg_height, self.wheelbase,
+                       self.actuator_tau, self.gravity, self.air_density, self.frontal_area)
+
+    @property
+    def max_steps(self) -> int:
+        # integrator.cpp:19 -- llround (half away from zero)
+        q = self.t_max / self.dt
+        return int(math.floor(abs(q) + 0.5)) * (1 if q >= 0 else -1)
+
+
+@dataclass
+class UncertaintyModel:
+    """sampling.hpp:24-33; stream order (initial_speed, friction, grade, mass, drag_coeff)."""
+    seed: int = 3
+    initial_speed: tuple = (30.0, 2.0)
+    friction: tuple = (0.8, 0.1)
+    grade: tuple = (0.0, 0.05)
+    mass: tuple = (1500.0, 100.0)
+    drag_coeff: tuple = (0.3, 0.05)
+
+    def c(self) -> N.Model:
+        return N.Model(self.seed, N.Normal(*self.initial_speed), N.Normal(*self.friction),
+                       N.Normal(*self.grade), N.Normal(*self.mass), N.Normal(*self.drag_coeff))
+
+    @staticmethod
+    def mixed(seed: int = 3) -> "UncertaintyModel":
+        """C4: wet/icy friction spread, +-6% grade."""
+        return UncertaintyModel(seed=seed, friction=(0.45, 0.20), grade=(0.0, math.atan(0.06)))
+
+
+def _p(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+def draw_batch(model: UncertaintyModel, n: int, first: int = 0, threads: int = 0):
+    """draw_batch (sampling.cpp:67-100) on the host thread pool; returns
+    (samples[n] with SAMPLE_DTYPE, clamp_count).  ``first`` selects the
+    shard [first, first+n) of the counter-based stream."""
+    lib = N.load()
+    out = np.empty(n, dtype=SAMPLE_DTYPE)
+    clamps = C.c_uint64(0)
+    m = model.c()
+    N.check(lib.bmc_draw_range(C.byref(m), first, n, _p(out), C.byref(clamps), threads))
+    return out, int(clamps.value)
+
+
+def stage_terms(samples: np.ndarray, world: SimWorld = SimWorld(), threads: int = 0):
+    """RolloutTerms::from (dynamics.cpp:57-68), SoA: (v0, floor, drag, grade)."""
+    lib = N.load()
+    samples = np.ascontiguousarray(samples, dtype=SAMPLE_DTYPE)
+    n = samples.shape[0]
+    out = np.empty((4, n), dtype=np.float64)
+    w = world.c()
+    N.check(lib.bmc_stage_terms(_p(samples), n, C.byref(w), _p(out[0]), _p(out[1]), _p(out[2]),
+                                _p(out[3]), threads))
+    return out
+
+
+def device_count() -> int:
+    lib = N.load()
+    c = C.c_int(0)
+    rc = lib.bmc_device_count(C.byref(c))
+    return int(c.value) if rc == 0 else 0
+
+
+@dataclass
+class RunReport:
+    """ExecutionReport (backends.hpp:25-30) + timing breakdown."""
+    results: np.ndarray
+    wall_time_s: float
+    executor: str = "cuda"
+    worker_count: int = 1
+    kernel_ms: float = 0.0
+    predict_ms: float = 0.0
+    total_steps: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    launches: int = 0
+    chunks: int = 0
+
+
+class CudaExecutor:
+    """One device context (streams, actuator-table cache, scratch)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = N.load()
+        self.device = device
+        h = C.c_void_p()
+        N.check(self.lib.bmc_cuda_init(device, C.byref(h)))
+        self.ctx = h
+
+    def close(self):
+        if self.ctx:
+            self.lib.bmc_cuda_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        N.check(rc, self.ctx)
+
+    @staticmethod
+    def _opts(schedule="default", block_threads=0, table="auto", host_threads=0, chunk=0):
+        return N.RunOpts(SCHEDULE[schedule], block_threads, TABLE[table], host_threads, chunk)
+
+    # -------------------------------------------------------------- executor
+    def run(self, samples: np.ndarray, world: SimWorld = SimWorld(), out: np.ndarray = None,
+            **opts) -> RunReport:
+        """run_cuda: host AoS samples -> host AoS results (bit-identical to
+        run_sequential, backends.cpp:38-55).  Synchronous."""
+        samples = np.ascontiguousarray(samples, dtype=SAMPLE_DTYPE)
+        n = samples.shape[0]
+        if out is None:
+            out = np.empty(n, dtype=RESULT_DTYPE)
+        w = world.c()
+        o = self._opts(**opts)
+        info = N.RunInfo()
+        self._check(self.lib.bmc_cuda_run(self.ctx, _p(samples), n, C.byref(w), C.byref(o),
+                                          _p(out), C.byref(info)))
+        return RunReport(out, info.wall_s, "cuda", 1, info.kernel_ms, info.predict_ms,
+                         int(info.total_steps), int(info.h2d_bytes), int(info.d2h_bytes),
+                         int(info.launches), int(info.chunks))
+
+    def rollout_device(self, terms, outputs, world: SimWorld = SimWorld(), total_steps=None,
+                       stream=None, **opts) -> None:
+        """Device-resident rollout. terms: 4 float64 CUDA tensors (v0, floor,
+        drag, grade); outputs: (stop_distance f64, steps i32, hit_horizon u8)
+        CUDA tensors or None.  Enqueued on ``stream`` (torch stream or None)."""
+        n = int(terms[0].numel())
+        t = N.Terms(*[int(x.data_ptr()) for x in terms])
+        o = N.Outputs(*[int(x.data_ptr()) if x is not None else None for x in outputs])
+        w = world.c()
+        op = self._opts(**opts)
+        ts = C.c_void_p(int(total_steps.data_ptr())) if total_steps is not None else None
+        st = C.c_void_p(int(stream.cuda_stream)) if stream is not None else None
+        self._check(self.lib.bmc_cuda_rollout_device(self.ctx, C.byref(t), n, C.byref(w),
+                                                     C.byref(op), C.byref(o), ts, st))
+
+    def last_kernel_ms(self):
+        r, p = C.c_float(0), C.c_float(0)
+        self._check(self.lib.bmc_cuda_last_kernel_ms(self.ctx, C.byref(r), C.byref(p)))
+        return float(r.value), float(p.value)
+
+    def last_launches(self) -> int:
+        v = C.c_uint32(0)
+        self._check(self.lib.bmc_cuda_last_launches(self.ctx, C.byref(v)))
+        return int(v.value)
+
+    def sync(self):
+        self._check(self.lib.bmc_cuda_sync(self.ctx))
+
+    def fp64_peak(self, reps: int = 5):
+        """Measured FP64 DADD/DMUL op rate (ops/s) and the best probe time (ms)."""
+        ops, ms = C.c_double(0), C.c_double(0)
+        self._check(self.lib.bmc_cuda_fp64_peak(self.ctx, reps, C.byref(ops), C.byref(ms)))
+        return float(ops.value), float(ms.value)
+
+    @property
+    def stream_handle(self) -> int:
+        return int(self.lib.bmc_cuda_stream(self.ctx) or 0)
+
+    # ------------------------------------------------------------ statistics
+    def summarize(self, d, hz, bin_width: float = 2.0, hist_cap: int = 1 << 16):
+        """summarize (analysis.cpp:13-76) over device outputs."""
+        n = int(d.numel())
+        s = N.Summary()
+        hist = np.zeros(hist_cap, dtype=np.uint64)
+        self._check(self.lib.bmc_cuda_summarize(self.ctx, C.c_void_p(d.data_ptr()),
+                                                C.c_void_p(hz.data_ptr()) if hz is not None else None,
+                                                n, bin_width, C.byref(s), _p(hist), hist_cap))
+        out = {k: getattr(s, k) for k, _ in N.Summary._fields_ if k != "pad_"}
+        out["right_skewed"] = bool(out["right_skewed"])
+        out["histogram"] = hist[: s.bins].copy()
+        return out
+
+    def exceedance_counts(self, d, hz, headways: Sequence[float]) -> np.ndarray:
+        """#{hit_horizon or d > h} per headway (analysis.cpp:145-159 numerators)."""
+        n = int(d.numel())
+        h = np.ascontiguousarray(headways, dtype=np.float64)
+        counts = np.zeros(h.shape[0], dtype=np.uint64)
+        self._check(self.lib.bmc_cuda_exceedance(self.ctx, C.c_void_p(d.data_ptr()),
+                                                 C.c_void_p(hz.data_ptr()) if hz is not None else None,
+                                                 n, _p(h), h.shape[0], _p(counts)))
+        return counts
+
+    def order_stats(self, d, hz, ranks: Sequence[int], exclude_horizon: bool):
+        n = int(d.numel())
+        r = np.ascontiguousarray(ranks, dtype=np.uint64)
+        out = np.zeros(r.shape[0], dtype=np.float64)
+        cnt = C.c_uint64(0)
+        self._check(self.lib.bmc_cuda_order_stats(self.ctx, C.c_void_p(d.data_ptr()),
+                                                  C.c_void_p(hz.data_ptr()) if hz is not None else None,
+                                                  n, 1 if exclude_horizon else 0, _p(r), r.shape[0],
+                                                  _p(out), C.byref(cnt)))
+        return out, int(cnt.value)
+
+    def collision_probability(self, d, hz, headway: float) -> float:
+        if not headway >= 0.0:
+            raise N.ConfigError("risk.headway: must be >= 0")
+        c = self.exceedance_counts(d, hz, [headway])
+        return float(c[0]) / float(d.numel())
+
+    def min_safe_headway(self, d, hz, risk: float) -> float:
+        """analysis.cpp:161-194: nudged rank, order statistic among stoppers."""
+        return self.min_safe_headways(d, hz, [risk])[0]
+
+    def min_safe_headways(self, d, hz, risks: Sequence[float]):
+        n = int(d.numel())
+        if n == 0:
+            raise N.ConfigError("risk: needs at least one result")
+        ranks = []
+        for risk in risks:
+            if not (0.0 < risk < 1.0):
+                raise N.ConfigError("risk.level: must be strictly between 0 and 1")
+            raw = (1.0 - risk) * float(n)
+            ranks.append(int(math.ceil(raw - raw * 1e-12)))
+        vals, stopped = self.order_stats(d, hz, ranks, exclude_horizon=True)
+        return [float("inf") if rk > stopped else float(v) for rk, v in zip(ranks, vals)]
+
+    def build_risk_curve(self, d, hz, grid: Sequence[float], risk_levels: Sequence[float],
+                         closing_speed: float):
+        """build_risk_curve (analysis.cpp:203-228): one O(n log m) pass for the
+        whole grid instead of one O(n) rescan per grid point."""
+        n = float(d.numel())
+        counts = self.exceedance_counts(d, hz, grid)
+        probs = counts.astype(np.float64) / n
+        g = list(grid)
+        for i in range(1, len(g)):
+            if g[i] >= g[i - 1] and probs[i] > probs[i - 1]:
+                raise AssertionError("risk curve must be non-increasing in headway")
+        levels = sorted(risk_levels, reverse=True)
+        heads = self.min_safe_headways(d, hz, levels)
+        thr = [(r, h, ttc_for_headway(h, closing_speed)) for r, h in zip(levels, heads)]
+        return probs, thr
+
+
+def ttc_for_headway(headway_m: float, closing_speed_mps: float) -> float:
+    """analysis.cpp:196-201"""
+    if not closing_speed_mps > 0.0:
+        raise N.ConfigError("risk.closing_speed: must be > 0")
+    return headway_m / closing_speed_mps
+
+
+def headway_grid(start: float, stop: float, step: float):
+    """analysis.cpp:230-241"""
+    if not (step > 0.0) or not (stop >= start):
+        raise N.ConfigError("risk.grid: needs stop >= start and step > 0")
+    count = int(math.floor((stop - start) / step + 1e-9))
+    return [start + float(i) * step for i in range(count + 1)]

@@ -1,0 +1,140 @@
+// parity_main.cpp -- the reference's executor parity checks, re-run against
+// brakemc::run_cuda through the reference's own C++ API.
+//
+// Links the UNMODIFIED reference (oracle/_ref/libbrakemc_ref.so: draw_batch,
+// run_sequential, run_parallel, verify_consistency) and the product library
+// (libbrakemc_b200.so via include/brakemc/cuda_executor.hpp).  Mirrors:
+//   * acceptance criterion 1, backend_bit_exactness
+//     (tests/acceptance/acceptance_main.cpp:65-107): seeds {1,2,3} x
+//     n {1k, 12k, 100k}, pass and max_abs_deviation == 0.0;
+//   * test_backends.cpp:26-68: single-sample report, chunk/scheduling
+//     independence, repeat determinism, empty-batch ConfigError.
+// Exit 0 on success; prints one line per check.  Run by
+// tests/test_gpu_cpp.py on the GPU box.
+#include "brakemc/backends.hpp"
+#include "brakemc/cuda_executor.hpp"
+#include "brakemc/errors.hpp"
+#include "brakemc/sampling.hpp"
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+using namespace brakemc;
+
+namespace {
+
+int failures = 0;
+
+void check(bool ok, const std::string& what) {
+    std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", what.c_str());
+    if (!ok) ++failures;
+}
+
+SampleBatch batch_of(std::uint64_t seed, std::size_t n, bool mixed = false) {
+    UncertaintyModel m;
+    m.seed = seed;
+    if (mixed) {
+        m.friction = NormalSpec{0.45, 0.20};
+        m.grade = NormalSpec{0.0, std::atan(0.06)};
+    }
+    return draw_batch(m, n);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    const bool quick = argc > 1 && std::string(argv[1]) == "--quick";
+    const SimConfig cfg{};
+    const VehicleGeometry geo{};
+    const PhysicalConstants phys{};
+
+    // acceptance_main.cpp:65-107 (criterion 1) with run_cuda as the backend
+    for (std::uint64_t seed : {1ull, 2ull, 3ull}) {
+        for (std::size_t n : {std::size_t{1000}, std::size_t{12000}, std::size_t{100000}}) {
+            if (quick && n > 12000) continue;
+            const SampleBatch b = batch_of(seed, n);
+            const ExecutionReport ref = run_parallel(b, cfg, geo, phys, 0);
+            const ExecutionReport gpu = run_cuda(b, cfg, geo, phys);
+            const ConsistencyVerdict v = verify_consistency(ref, gpu);
+            check(v.pass && v.max_abs_deviation == 0.0 && v.bitwise_equal &&
+                      gpu.worker_count == 1 && gpu.executor == kCudaExecutorKind,
+                  "criterion1 seed=" + std::to_string(seed) + " n=" + std::to_string(n));
+        }
+    }
+
+    // mixed-condition (divergence-heavy, ~27% horizon hits) batch
+    {
+        const SampleBatch b = batch_of(3, quick ? 20000 : 100000, true);
+        const ExecutionReport ref = run_parallel(b, cfg, geo, phys, 0);
+        const ExecutionReport gpu = run_cuda(b, cfg, geo, phys);
+        check(verify_consistency(ref, gpu).pass, "mixed model bit-exact");
+    }
+
+    // test_backends.cpp:26-36: a single-sample report equals the rollout
+    {
+        const SampleBatch b = batch_of(3, 1);
+        const ExecutionReport gpu = run_cuda(b, cfg, geo, phys);
+        const RolloutResult direct = simulate_rollout(b.samples[0], cfg, geo, phys);
+        check(gpu.results.size() == 1 && gpu.results[0].stop_distance == direct.stop_distance &&
+                  gpu.results[0].steps == direct.steps &&
+                  gpu.results[0].stop_time == direct.stop_time &&
+                  gpu.results[0].hit_horizon == direct.hit_horizon,
+              "single-sample report equals simulate_rollout");
+    }
+
+    // test_backends.cpp:52-68: scheduling knobs never change results
+    {
+        const SampleBatch b = batch_of(5, 7000, true);
+        const ExecutionReport ref = run_sequential(b, cfg, geo, phys);
+        bool all = true;
+        for (int sched : {1, 2}) {
+            for (int tm : {1, 2, 3}) {
+                for (std::size_t chunk : {std::size_t{0}, std::size_t{999}}) {
+                    CudaExecOptions o;
+                    o.schedule = sched;
+                    o.table_mode = tm;
+                    o.chunk_samples = chunk;
+                    o.block_threads = tm == 3 ? 256 : 512;
+                    all = all && verify_consistency(ref, run_cuda(b, cfg, geo, phys, o)).pass;
+                }
+            }
+        }
+        check(all, "schedule / table mode / chunk independence");
+        const ExecutionReport a1 = run_cuda(b, cfg, geo, phys);
+        const ExecutionReport a2 = run_cuda(b, cfg, geo, phys);
+        check(verify_consistency(a1, a2).pass, "repeated runs identical");
+    }
+
+    // non-default configs (horizon shorter than the actuator fixed point, etc.)
+    {
+        const SampleBatch b = batch_of(8, 3000, true);
+        bool all = true;
+        SimConfig c2 = cfg;
+        c2.t_max = 3.0;  // max_steps 3000 < actuator fixed point (4803)
+        VehicleGeometry g2 = geo;
+        g2.actuator_tau = 0.4;
+        SimConfig c3 = cfg;
+        c3.dt = 0.002;
+        c3.brake_cmd = -8.0;
+        all = all && verify_consistency(run_sequential(b, c2, geo, phys), run_cuda(b, c2, geo, phys)).pass;
+        all = all && verify_consistency(run_sequential(b, cfg, g2, phys), run_cuda(b, cfg, g2, phys)).pass;
+        all = all && verify_consistency(run_sequential(b, c3, geo, phys), run_cuda(b, c3, geo, phys)).pass;
+        check(all, "non-default SimConfig / geometry bit-exact");
+    }
+
+    // backends.cpp:41-43: empty batch -> ConfigError with the field path
+    {
+        bool threw = false;
+        try {
+            run_cuda(SampleBatch{}, cfg, geo, phys);
+        } catch (const ConfigError& e) {
+            threw = std::string(e.what()) == "batch: must be non-empty";
+        }
+        check(threw, "empty batch throws ConfigError(batch)");
+    }
+
+    std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
+    return failures ? 1 : 0;
+}

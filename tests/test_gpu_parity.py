@@ -1,0 +1,166 @@
+"""GPU parity: the CUDA executor vs the reference, bit for bit.
+
+Every test calls the product through the C-ABI (libbrakemc_b200.so) and
+compares with the reference library (oracle/_ref) run on the SAME samples on
+the same host, so glibc-libm variance cannot leak in.  Bar: bitwise equality
+of all four RolloutResult fields (backends.cpp:24-30), i.e. the reference's
+verify_consistency verdict `pass` with max_abs_deviation == 0.0.
+"""
+import math
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2604_27193_b200 as bmc
+from oracle.pyoracle import Model, World, results_bitwise_equal
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def to_model(m: Model) -> bmc.UncertaintyModel:
+    return bmc.UncertaintyModel(m.seed, *zip(m.mean, m.sd))
+
+
+def to_world(w: World) -> bmc.SimWorld:
+    return bmc.SimWorld(*w.as_array().tolist())
+
+
+def assert_parity(ref, want, got):
+    v = ref.verify_consistency(want, got)
+    assert v["passed"] and v["max_abs_deviation"] == 0.0, v
+    assert results_bitwise_equal(want, got)
+
+
+# acceptance_main.cpp:65-107 -- criterion 1 matrix
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("n", [1000, 12000, 100000])
+def test_criterion1_matrix(ref, executor, seed, n):
+    samples, _ = ref.draw_batch(Model(seed=seed), n)
+    want, _, _ = ref.run(samples, World(), "parallel")
+    rep = executor.run(samples)
+    assert_parity(ref, want, rep.results)
+    assert rep.total_steps == int(want["steps"].sum())
+
+
+def test_mixed_model_with_horizons(ref, executor):
+    samples, _ = ref.draw_batch(Model.mixed(3), 100000)
+    want, _, _ = ref.run(samples, World(), "parallel")
+    assert want["hit_horizon"].mean() > 0.2  # divergence-heavy: ~27% horizon
+    rep = executor.run(samples)
+    assert_parity(ref, want, rep.results)
+
+
+@pytest.mark.parametrize("schedule", ["index", "binned"])
+@pytest.mark.parametrize("table", ["shared", "global", "none"])
+@pytest.mark.parametrize("block", [256, 512, 1024])
+def test_scheduling_knobs_never_change_bits(ref, executor, schedule, table, block):
+    samples, _ = ref.draw_batch(Model.mixed(17), 6000)
+    want, _, _ = ref.run(samples, World(), "parallel")
+    rep = executor.run(samples, schedule=schedule, table=table, block_threads=block,
+                       chunk=2500)
+    assert_parity(ref, want, rep.results)
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 257])
+def test_ragged_sizes(ref, executor, n):
+    samples, _ = ref.draw_batch(Model.mixed(n), n)
+    want, _, _ = ref.run(samples, World(), "sequential")
+    assert_parity(ref, want, executor.run(samples).results)
+
+
+def test_empty_batch_is_config_error(executor):
+    with pytest.raises(bmc.ConfigError, match="batch: must be non-empty"):
+        executor.run(np.zeros(0, dtype=bmc.SAMPLE_DTYPE))
+
+
+def test_domain_error(executor):
+    s = np.zeros(1, dtype=bmc.SAMPLE_DTYPE)
+    s[0] = (30.0, 0.8, 0.0, 1500.0, 0.3)
+    with pytest.raises(bmc.DomainError):
+        executor.run(s, bmc.SimWorld(wheelbase=-0.2))
+
+
+WORLDS = [
+    World(t_max=3.0),                               # horizon before the actuator fixed point
+    World(dt=0.002, brake_cmd=-8.0),
+    World(actuator_tau=0.4),
+    World(actuator_tau=30.0),                       # no fixed point inside the horizon
+    World(dt=0.0005, t_max=6.0, gravity=9.7, air_density=1.1, frontal_area=2.6),
+    World(t_max=0.0005),                            # llround(0.5) = 1 step
+    World(t_max=0.0),                               # zero steps: all horizon
+]
+
+
+@pytest.mark.parametrize("w", WORLDS, ids=lambda w: f"dt{w.dt}_tmax{w.t_max}_tau{w.actuator_tau}")
+def test_nondefault_worlds(ref, executor, w):
+    samples, _ = ref.draw_batch(Model.mixed(23), 3000)
+    want, _, _ = ref.run(samples, w, "parallel")
+    assert_parity(ref, want, executor.run(samples, to_world(w)).results)
+
+
+def test_known_answer_cases(ref, executor):
+    # test_integrator.cpp: nominal (5079 steps), weak grip, glare ice horizon,
+    # mu threshold flat region, extreme clamps
+    rows = [(30.0, 0.8, 0.0, 1500.0, 0.3), (30.0, 0.5, 0.0, 1500.0, 0.3),
+            (30.0, 0.05, -0.3, 1500.0, 0.3), (30.0, 0.6997432622301698, 0.0, 1500.0, 0.3),
+            (30.0, 1.2, 0.0, 1500.0, 0.3), (0.1, 0.05, 1.5, 500.0, 0.0),
+            (45.0, 0.05, -1.5, 500.0, 0.6), (0.1, 3.0, 0.0, 4000.0, 0.0)]
+    s = np.array(rows, dtype=bmc.SAMPLE_DTYPE)
+    want, _, _ = ref.run(s, World(), "sequential")
+    got = executor.run(s).results
+    assert_parity(ref, want, got)
+    assert got[0]["steps"] == 5079 and got[2]["hit_horizon"] == 1
+    assert got[3]["stop_distance"] == got[4]["stop_distance"]
+
+
+def test_constant_deceleration_long_rollout(ref, executor):
+    # test_integrator.cpp:106-119: dt = tau = 1e-6, 5,000,002 steps
+    w = World(air_density=0.0, actuator_tau=1e-6, dt=1e-6)
+    s = np.array([(30.0, 0.8, 0.0, 1500.0, 0.3)], dtype=bmc.SAMPLE_DTYPE)
+    want, _, _ = ref.run(s, w, "sequential")
+    got = executor.run(s, to_world(w)).results
+    assert_parity(ref, want, got)
+    assert got[0]["stop_distance"] == pytest.approx(75.0, abs=0.01)
+
+
+def test_host_sampler_feeds_gpu(ref, executor):
+    # product sampler (host pool) -> GPU == reference sampler -> reference
+    mine, _ = bmc.draw_batch(bmc.UncertaintyModel(seed=9), 20000)
+    theirs, _ = ref.draw_batch(Model(seed=9), 20000)
+    assert np.array_equal(mine.view(np.uint64), theirs.view(np.uint64))
+    want, _, _ = ref.run(theirs, World(), "parallel")
+    assert_parity(ref, want, executor.run(mine).results)
+
+
+def test_device_resident_path(ref, executor):
+    import torch
+    samples, _ = ref.draw_batch(Model.mixed(31), 50000)
+    want, _, _ = ref.run(samples, World(), "parallel")
+    terms = bmc.stage_terms(samples)
+    dev = [torch.from_numpy(terms[i].copy()).cuda() for i in range(4)]
+    n = samples.shape[0]
+    d = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = torch.empty(n, dtype=torch.int32, device="cuda")
+    hz = torch.empty(n, dtype=torch.uint8, device="cuda")
+    total = torch.zeros(1, dtype=torch.int64, device="cuda")
+    executor.rollout_device(dev, (d, st, hz), total_steps=total)
+    executor.sync()
+    assert np.array_equal(d.cpu().numpy().view(np.uint64), want["stop_distance"].view(np.uint64))
+    assert np.array_equal(st.cpu().numpy().astype(np.int64), want["steps"])
+    assert np.array_equal(hz.cpu().numpy(), want["hit_horizon"])
+    assert int(total.item()) == int(want["steps"].sum())
+    rms, pms = executor.last_kernel_ms()
+    assert rms > 0.0
+    assert executor.last_launches() == 4  # predict, scan, scatter, rollout
+
+
+def test_cpp_executor_api():
+    """The reference's own C++ parity checks through brakemc::run_cuda."""
+    exe = os.path.join(ROOT, "build", "parity_cpp")
+    assert os.path.exists(exe), "build/parity_cpp missing (built by __graft_entry__.build())"
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(p.stdout)
+    assert p.returncode == 0, p.stdout + p.stderr
