@@ -158,6 +158,10 @@ int bmc_cuda_rollout_device(bmc_ctx* ctx, const bmc_terms* terms, size_t n,
 /* Last rollout kernel's device time in ms, via CUDA events recorded around
  * it on its own stream (valid after the stream is synchronised). */
 int bmc_cuda_last_kernel_ms(bmc_ctx* ctx, float* rollout_ms, float* predict_ms);
+/* Executed RK4 steps and lane slots (sum over 32-sample groups of
+ * active lanes x longest lane) of the last rollout launch on the context's
+ * stream; steps / slots is the SIMT lane efficiency.  Synchronises. */
+int bmc_cuda_last_lane_stats(bmc_ctx* ctx, uint64_t* steps, uint64_t* slots);
 /* Number of kernels the last device call enqueued. */
 int bmc_cuda_last_launches(bmc_ctx* ctx, uint32_t* launches);
 

@@ -21,7 +21,7 @@ namespace {
 constexpr size_t kTableCap = size_t{1} << 20;      // 32 MB of stage values
 constexpr uint64_t kDefaultChunk = uint64_t{1} << 22;  // 4M samples per pipeline slot
 constexpr int kMaxCoarseSteps = 2048;
-constexpr int kBucketsTarget = 2048;
+constexpr int kBucketsTarget = 2000;  // step buckets; x2 clamp classes <= 4096 keys
 
 bool same_key(const WorldDerived& a, const WorldDerived& b) {
     return std::memcmp(&a, &b, sizeof a) == 0;
@@ -31,10 +31,27 @@ int ensure_table(bmc_ctx* ctx, const WorldDerived& d) {
     if (ctx->have_table && same_key(ctx->tkey, d)) return BMC_OK;
     const ActuatorTable t = build_actuator_table(d, kTableCap);
     ctx->have_table = false;
-    ctx->t_converged = t.converged;
+    // The kernel's crossover form of the clamp needs every stage sequence to
+    // be non-increasing in n (true whenever brake_cmd < 0 and the RK4 step is
+    // stable); anything else runs the generic inline path.
+    bool monotone = true;
+    double tmin = t.stages.empty() ? 0.0 : t.stages[0].a0;
+    for (size_t k = 0; k < t.stages.size(); ++k) {
+        const StageA& e = t.stages[k];
+        for (double vv : {e.a0, e.a1, e.a2, e.a3}) {
+            if (!(vv == vv)) monotone = false;
+            tmin = std::min(tmin, vv);
+        }
+        if (k > 0) {
+            const StageA& p = t.stages[k - 1];
+            if (e.a0 > p.a0 || e.a1 > p.a1 || e.a2 > p.a2 || e.a3 > p.a3) monotone = false;
+        }
+    }
+    ctx->t_converged = t.converged && monotone;
+    ctx->t_min = tmin;
     ctx->t_len = static_cast<int>(t.stages.size());
     ctx->coarse_len = 0;
-    if (t.converged) {
+    if (ctx->t_converged) {
         const size_t bytes = t.stages.size() * sizeof(StageA);
         BMC_CK(ctx, ctx->d_table.reserve(bytes));
         BMC_CK(ctx, cudaMemcpy(ctx->d_table.p, t.stages.data(), bytes, cudaMemcpyHostToDevice));
@@ -83,14 +100,14 @@ int enqueue_rollout(bmc_ctx* ctx, const bmc_terms& terms, uint64_t n, const Worl
     if (ctx->coarse_len == 0 || mode == kTableNone) sched = kScheduleIndex;
 
     int bt = opts.block_threads;
-    if (bt == 0) bt = 512;
+    if (bt == 0) bt = mode == kTableGlobal ? 256 : 1024;
 
     uint32_t nl = 0;
     const uint32_t* perm = nullptr;
     ev.predicted = false;
     if (sched == kScheduleBinned && n > 0) {
         const int width = static_cast<int>((d.max_steps + kBucketsTarget) / kBucketsTarget);
-        const int buckets = static_cast<int>(d.max_steps / width) + 1;
+        const int buckets = 2 * (static_cast<int>(d.max_steps / width) + 1);
         BMC_CK(ctx, ctx->keys.reserve(n * sizeof(uint16_t)));
         BMC_CK(ctx, ctx->perm.reserve(n * sizeof(uint32_t)));
         BMC_CK(ctx, ctx->hist.reserve(4096 * sizeof(unsigned int)));
@@ -109,6 +126,7 @@ int enqueue_rollout(bmc_ctx* ctx, const bmc_terms& terms, uint64_t n, const Worl
         pa.max_steps = static_cast<int32_t>(d.max_steps);
         pa.bucket_width = width;
         pa.buckets = buckets;
+        pa.table_min = ctx->t_min;
         pa.keys = ctx->keys.as<uint16_t>();
         pa.hist = ctx->hist.as<unsigned int>();
         BMC_CK(ctx, launch_predict(pa, s));
@@ -121,8 +139,9 @@ int enqueue_rollout(bmc_ctx* ctx, const bmc_terms& terms, uint64_t n, const Worl
         ev.predicted = true;
     }
 
-    BMC_CK(ctx, ctx->counter.reserve(sizeof(unsigned int)));
-    BMC_CK(ctx, cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned int), s));
+    // [0] work counter (u32) | [8] executed steps (u64) | [16] lane slots (u64)
+    BMC_CK(ctx, ctx->counter.reserve(64));
+    BMC_CK(ctx, cudaMemsetAsync(ctx->counter.p, 0, 24, s));
     RolloutArgs ra{};
     ra.v0 = terms.initial_speed;
     ra.brake_floor = terms.brake_floor;
@@ -143,6 +162,7 @@ int enqueue_rollout(bmc_ctx* ctx, const bmc_terms& terms, uint64_t n, const Worl
     ra.hit_horizon = out.hit_horizon;
     ra.total_steps = total_steps_dev;
     ra.work_counter = ctx->counter.as<unsigned int>();
+    ra.counters = reinterpret_cast<unsigned long long*>(ctx->counter.as<char>() + 8);
     BMC_CK(ctx, cudaEventRecord(ev.r0, s));
     if (n > 0) {
         BMC_CK(ctx, launch_rollout(ra, mode, bt, s));
@@ -300,6 +320,19 @@ int bmc_cuda_fp64_peak(bmc_ctx* ctx, int reps, double* ops_per_s, double* best_m
     }
     if (ops_per_s) *ops_per_s = static_cast<double>(ops) / (best * 1e-3);
     if (best_ms) *best_ms = best;
+    return BMC_OK;
+}
+
+int bmc_cuda_last_lane_stats(bmc_ctx* ctx, uint64_t* steps, uint64_t* slots) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    unsigned long long c[2] = {0, 0};
+    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->counter.p) {
+        BMC_CK(ctx, cudaMemcpy(c, ctx->counter.as<char>() + 8, sizeof c, cudaMemcpyDeviceToHost));
+    }
+    if (steps) *steps = c[0];
+    if (slots) *slots = c[1];
     return BMC_OK;
 }
 

@@ -95,6 +95,7 @@ struct bmc_ctx {
     bool have_table = false;
     bmc::WorldDerived tkey{};
     bool t_converged = false;
+    double t_min = 0.0;
     int t_len = 0;
     bmc::DevBuf d_table, d_coarse;
     int coarse_len = 0;

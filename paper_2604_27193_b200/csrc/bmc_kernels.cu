@@ -23,6 +23,8 @@
 
 #include <cub/block/block_scan.cuh>
 
+#include <climits>
+
 namespace bmc {
 namespace {
 
@@ -87,62 +89,109 @@ __device__ __forceinline__ StageA load_stage(const StageA* tab, int n) {
     }
 }
 
-// simulate_rollout (integrator.cpp:13-29) for sample j.
+// v <= 0.0 (integrator.cpp:22) on the integer pipe: a binary64 pattern read
+// as int64 is <= 0 exactly for +0, -0 and every negative value, so the test
+// agrees with the FP compare for every non-NaN v and leaves the FP64 pipe to
+// the RK4 arithmetic.  (Only a sign-bit-set NaN would differ; finite inputs
+// cannot produce one.)
+__device__ __forceinline__ bool not_positive(double v) { return __double_as_longlong(v) <= 0ll; }
+
 template <int MODE>
-__device__ __forceinline__ int32_t run_one(const RolloutArgs& A, const StageA* tab, int len,
-                                           uint64_t j) {
+__device__ __forceinline__ double stage_value(const StageA* tab, int n, int s) {
+    const double* p = reinterpret_cast<const double*>(tab) + 4 * n + s;
+    return MODE == kTableGlobal ? __ldg(p) : *p;
+}
+
+// First step n at which clamp_brake(A_s[n], F) == F, i.e. !(A_s[n] > F).
+// The host only hands over tables that are non-increasing in n for every
+// stage, so the predicate is monotone and clamp_brake(A_s[n], F) equals
+// (n < c_s ? A_s[n] : F) for every n -- bit for bit, including NaN F.
+template <int MODE>
+__device__ __forceinline__ int crossover(const StageA* tab, int len, int s, double F) {
+    int lo = 0, hi = len;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (stage_value<MODE>(tab, mid, s) > F) {
+            lo = mid + 1;
+        } else {
+            hi = mid;
+        }
+    }
+    return lo == len ? INT_MAX : lo;
+}
+
+struct LaneOut {
+    double x;
+    int32_t steps;
+    bool stopped;
+};
+
+// simulate_rollout (integrator.cpp:13-29) for sample j, table modes.  The
+// step loop is split at warp-uniform bounds so that almost every step runs
+// a body with no clamp selects at all:
+//   V1 [0, cmin_w)       brake = table stage values      (no lane clamped yet)
+//   V2 [cmin_w, cmax_w)  brake = n < c_s ? table : floor (crossover band)
+//   V3 [.., max_steps)   brake = per-lane constants      (all lanes clamped, or
+//                        past the actuator fixed point)
+template <int MODE>
+__device__ __forceinline__ LaneOut run_table(const RolloutArgs& A, const StageA* tab, int len,
+                                             uint64_t j, unsigned mask) {
     const double D = A.drag[j];
     const double G = A.grade[j];
     const double F = A.brake_floor[j];
     double v = A.v0[j];
     double x = 0.0;
     const int32_t M = A.max_steps;
+    const int c0 = crossover<MODE>(tab, len, 0, F), c1 = crossover<MODE>(tab, len, 1, F);
+    const int c2 = crossover<MODE>(tab, len, 2, F), c3 = crossover<MODE>(tab, len, 3, F);
+    const int cmin = min(min(c0, c1), min(c2, c3));
+    const int cmax = max(max(c0, c1), max(c2, c3));
+    const int head = min(len - 1, M);
+    const int p1 = min(static_cast<int>(__reduce_min_sync(mask, static_cast<unsigned>(cmin))), head);
+    const int p2 = min(static_cast<int>(__reduce_max_sync(mask, static_cast<unsigned>(cmax))), head);
     int32_t n = 0;
-    bool stopped = false;
-    if (MODE == kTableNone) {
-        double a = 0.0;
+    for (; n < p1; ++n) {
+        const StageA s = load_stage<MODE>(tab, n);
+        rk4_xv(x, v, s.a0, s.a1, s.a2, s.a3, D, G, A.dt, A.half, A.sixth);
+        if (not_positive(v)) return LaneOut{x, n + 1, true};
+    }
+    for (; n < p2; ++n) {
+        const StageA s = load_stage<MODE>(tab, n);
+        rk4_xv(x, v, n < c0 ? s.a0 : F, n < c1 ? s.a1 : F, n < c2 ? s.a2 : F,
+               n < c3 ? s.a3 : F, D, G, A.dt, A.half, A.sixth);
+        if (not_positive(v)) return LaneOut{x, n + 1, true};
+    }
+    if (n < M) {
+        const StageA s = load_stage<MODE>(tab, len - 1);
+        const double b0 = c0 <= n ? F : s.a0, b1 = c1 <= n ? F : s.a1;
+        const double b2 = c2 <= n ? F : s.a2, b3 = c3 <= n ? F : s.a3;
         for (; n < M; ++n) {
-            double an;
-            const StageA s = actuator_stages(a, A.brake_cmd, A.inv_tau, A.dt, A.half, A.sixth, &an);
-            rk4_xv(x, v, clamp_brake(s.a0, F), clamp_brake(s.a1, F), clamp_brake(s.a2, F),
-                   clamp_brake(s.a3, F), D, G, A.dt, A.half, A.sixth);
-            a = an;
-            if (v <= 0.0) {
-                stopped = true;
-                break;
-            }
-        }
-    } else {
-        const int32_t head = min(len - 1, M);
-        for (; n < head; ++n) {
-            const StageA s = load_stage<MODE>(tab, n);
-            rk4_xv(x, v, clamp_brake(s.a0, F), clamp_brake(s.a1, F), clamp_brake(s.a2, F),
-                   clamp_brake(s.a3, F), D, G, A.dt, A.half, A.sixth);
-            if (v <= 0.0) {
-                stopped = true;
-                break;
-            }
-        }
-        if (!stopped && n < M) {
-            // Past the actuator fixed point every stage value is constant,
-            // hence so are the clamped brake values of this lane.
-            const StageA s = load_stage<MODE>(tab, len - 1);
-            const double b1 = clamp_brake(s.a0, F), b2 = clamp_brake(s.a1, F);
-            const double b3 = clamp_brake(s.a2, F), b4 = clamp_brake(s.a3, F);
-            for (; n < M; ++n) {
-                rk4_xv(x, v, b1, b2, b3, b4, D, G, A.dt, A.half, A.sixth);
-                if (v <= 0.0) {
-                    stopped = true;
-                    break;
-                }
-            }
+            rk4_xv(x, v, b0, b1, b2, b3, D, G, A.dt, A.half, A.sixth);
+            if (not_positive(v)) return LaneOut{x, n + 1, true};
         }
     }
-    const int32_t steps = stopped ? n + 1 : M;
-    if (A.stop_distance) A.stop_distance[j] = x;
-    if (A.steps) A.steps[j] = steps;
-    if (A.hit_horizon) A.hit_horizon[j] = stopped ? 0 : 1;
-    return steps;
+    return LaneOut{x, M, false};
+}
+
+// Generic path (no usable table): the actuator lane is integrated inline
+// exactly as the reference does, with the ternary clamp on every stage.
+__device__ __forceinline__ LaneOut run_inline(const RolloutArgs& A, uint64_t j) {
+    const double D = A.drag[j];
+    const double G = A.grade[j];
+    const double F = A.brake_floor[j];
+    double v = A.v0[j];
+    double x = 0.0;
+    double a = 0.0;
+    const int32_t M = A.max_steps;
+    for (int32_t n = 0; n < M; ++n) {
+        double an;
+        const StageA s = actuator_stages(a, A.brake_cmd, A.inv_tau, A.dt, A.half, A.sixth, &an);
+        rk4_xv(x, v, clamp_brake(s.a0, F), clamp_brake(s.a1, F), clamp_brake(s.a2, F),
+               clamp_brake(s.a3, F), D, G, A.dt, A.half, A.sixth);
+        a = an;
+        if (v <= 0.0) return LaneOut{x, n + 1, true};
+    }
+    return LaneOut{x, M, false};
 }
 
 template <int MODE, int BT>
@@ -158,7 +207,7 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
         tab = reinterpret_cast<const StageA*>(smem_raw);
     }
     const unsigned lane = threadIdx.x & 31u;
-    unsigned long long my_steps = 0;
+    unsigned long long my_steps = 0, my_slots = 0;
     for (;;) {
         unsigned g = 0;
         if (lane == 0) g = atomicAdd(A.work_counter, 1u);
@@ -166,14 +215,32 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
         const uint64_t base = static_cast<uint64_t>(g) * 32u;
         if (base >= A.n) break;
         const uint64_t i = base + lane;
+        const unsigned mask = __ballot_sync(0xffffffffu, i < A.n);
         if (i < A.n) {
             const uint64_t j = A.perm ? static_cast<uint64_t>(A.perm[i]) : i;
-            my_steps += static_cast<unsigned long long>(max(run_one<MODE>(A, tab, len, j), 0));
+            const LaneOut r = MODE == kTableNone ? run_inline(A, j) : run_table<MODE>(A, tab, len, j, mask);
+            if (A.stop_distance) A.stop_distance[j] = r.x;
+            if (A.steps) A.steps[j] = r.steps;
+            if (A.hit_horizon) A.hit_horizon[j] = r.stopped ? 0 : 1;
+            const unsigned st = static_cast<unsigned>(max(r.steps, 0));
+            my_steps += st;
+            // lane-efficiency bookkeeping: the warp ran max(steps) slots per lane
+            const unsigned gmax = __reduce_max_sync(mask, st);
+            if (lane == static_cast<unsigned>(__ffs(mask) - 1)) {
+                my_slots += static_cast<unsigned long long>(gmax) * __popc(mask);
+            }
         }
     }
-    if (A.total_steps) {
-        for (int o = 16; o > 0; o >>= 1) my_steps += __shfl_down_sync(0xffffffffu, my_steps, o);
-        if (lane == 0 && my_steps) atomicAdd(A.total_steps, my_steps);
+    for (int o = 16; o > 0; o >>= 1) {
+        my_steps += __shfl_down_sync(0xffffffffu, my_steps, o);
+        my_slots += __shfl_down_sync(0xffffffffu, my_slots, o);
+    }
+    if (lane == 0) {
+        if (A.total_steps && my_steps) atomicAdd(A.total_steps, my_steps);
+        if (A.counters) {
+            atomicAdd(&A.counters[0], my_steps);
+            atomicAdd(&A.counters[1], my_slots);
+        }
     }
 }
 
@@ -222,7 +289,11 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictArgs P) {
             v = vn;
         }
         pred = max(1, min(pred, P.max_steps));
-        const int bucket = min((P.max_steps - pred) / P.bucket_width, P.buckets - 1);
+        // key = (descending step bucket, clamp class): warps see one class,
+        // so the never-clamping majority runs the select-free loop body
+        const int sb = (P.max_steps - pred) / P.bucket_width;
+        const int cls = P.brake_floor[i] < P.table_min ? 0 : 1;
+        const int bucket = min(2 * sb + cls, P.buckets - 1);
         P.keys[i] = static_cast<uint16_t>(bucket);
         atomicAdd(&s_hist[bucket], 1u);
     }

@@ -30,6 +30,7 @@ struct RolloutArgs {
     uint8_t* hit_horizon;  // nullable
     unsigned long long* total_steps;  // nullable
     unsigned int* work_counter;       // device, zeroed before launch
+    unsigned long long* counters;     // nullable: [0] executed steps, [1] lane slots
 };
 
 struct PredictArgs {
@@ -44,7 +45,8 @@ struct PredictArgs {
     float inv_dt;
     int32_t max_steps;
     int32_t bucket_width;   // steps per bucket
-    int32_t buckets;
+    int32_t buckets;        // total keys = 2 * step buckets (clamp class bit)
+    double table_min;       // min actuator stage value: F < table_min never clamps
     uint16_t* keys;         // out: bucket per sample (descending predicted steps)
     unsigned int* hist;     // out: per-bucket counts (zeroed before launch)
 };

@@ -191,6 +191,12 @@ class CudaExecutor:
         self._check(self.lib.bmc_cuda_last_kernel_ms(self.ctx, C.byref(r), C.byref(p)))
         return float(r.value), float(p.value)
 
+    def lane_efficiency(self):
+        """(executed steps, lane slots, efficiency) of the last rollout launch."""
+        a, b = C.c_uint64(0), C.c_uint64(0)
+        self._check(self.lib.bmc_cuda_last_lane_stats(self.ctx, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value), (a.value / b.value if b.value else 0.0)
+
     def last_launches(self) -> int:
         v = C.c_uint32(0)
         self._check(self.lib.bmc_cuda_last_launches(self.ctx, C.byref(v)))

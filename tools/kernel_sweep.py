@@ -59,10 +59,11 @@ def main():
                 best = (r, p)
         steps = int(tot.item())
         r, p = best
+        _, _, eff = ex.lane_efficiency()
         print(f"{a.model:7s} n={n} sched={sched:6s} table={table:6s} bt={bt:4d}  "
               f"rollout {r:9.3f} ms  predict {p:7.3f} ms  steps/s {steps/(r*1e-3):.4e}  "
               f"exec-op/s {32*steps/(r*1e-3)/1e12:.3f} T ({32*steps/(r*1e-3)/peak:.3f} of probe)"
-              f"  algo {57*steps/(r*1e-3)/peak:.3f}", flush=True)
+              f"  algo {57*steps/(r*1e-3)/peak:.3f}  lane-eff {eff:.4f}", flush=True)
 
 
 if __name__ == "__main__":
