@@ -147,6 +147,32 @@ int bmc_stage_terms(const bmc_sample* samples, size_t n, const bmc_world* world,
 int bmc_cuda_run(bmc_ctx* ctx, const bmc_sample* samples, size_t n, const bmc_world* world,
                  const bmc_run_opts* opts, bmc_result* out, bmc_run_info* info);
 
+/* Model-driven streaming executor (no AoS batch is ever materialised):
+ * samples [first, first+n) of draw_batch(model, .) are drawn by the host pool
+ * straight into pinned SoA terms, streamed H2D per chunk on a side stream and
+ * overlapped with the kernels of the previous chunk.  Exactly one of
+ * host_out (AoS results, RolloutResult layout) or dev_out (device-resident
+ * compact outputs with n entries each -- stats-only mode for 1e9-sample
+ * runs) must be non-NULL.  clamp_count = draw_batch's clamp_count. */
+int bmc_cuda_run_model(bmc_ctx* ctx, const bmc_model* model, uint64_t first, size_t n,
+                       const bmc_world* world, const bmc_run_opts* opts, bmc_result* host_out,
+                       const bmc_outputs* dev_out, uint64_t* clamp_count, bmc_run_info* info);
+
+/* Real-time mode (C2): a fixed-size decision batch captured once as a CUDA
+ * graph {H2D terms, predict/bin, rollout, D2H outputs}; each decision is
+ * host staging + one cudaGraphLaunch + unpack.  The graph owns its buffers. */
+typedef struct bmc_graph bmc_graph;
+int bmc_cuda_graph_create(bmc_ctx* ctx, size_t n, const bmc_world* world,
+                          const bmc_run_opts* opts, bmc_graph** out);
+int bmc_cuda_graph_run(bmc_graph* g, const bmc_sample* samples, bmc_result* out,
+                       bmc_run_info* info);
+/* Same, drawing the n samples [first, first+n) of `model` on the host pool
+ * (the reference's feasibility convention includes sampling,
+ * analysis.cpp:331-338). */
+int bmc_cuda_graph_run_model(bmc_graph* g, const bmc_model* model, uint64_t first,
+                             bmc_result* out, uint64_t* clamp_count, bmc_run_info* info);
+void bmc_cuda_graph_destroy(bmc_graph* g);
+
 /* Device-resident rollout: terms and outputs are device pointers; enqueued
  * on `stream` (NULL = the context's stream); returns without synchronising.
  * total_steps_dev (device uint64, nullable) accumulates executed steps. */

@@ -108,6 +108,16 @@ SIGNATURES = [
     ("bmc_stage_terms", C.c_int, [_P, C.c_size_t, C.POINTER(World), _P, _P, _P, _P, C.c_int]),
     ("bmc_cuda_run", C.c_int, [_P, _P, C.c_size_t, C.POINTER(World), C.POINTER(RunOpts), _P,
                                C.POINTER(RunInfo)]),
+    ("bmc_cuda_run_model", C.c_int, [_P, C.POINTER(Model), C.c_uint64, C.c_size_t,
+                                     C.POINTER(World), C.POINTER(RunOpts), _P,
+                                     C.POINTER(Outputs), C.POINTER(C.c_uint64),
+                                     C.POINTER(RunInfo)]),
+    ("bmc_cuda_graph_create", C.c_int, [_P, C.c_size_t, C.POINTER(World), C.POINTER(RunOpts),
+                                        C.POINTER(_P)]),
+    ("bmc_cuda_graph_run", C.c_int, [_P, _P, _P, C.POINTER(RunInfo)]),
+    ("bmc_cuda_graph_run_model", C.c_int, [_P, C.POINTER(Model), C.c_uint64, _P,
+                                           C.POINTER(C.c_uint64), C.POINTER(RunInfo)]),
+    ("bmc_cuda_graph_destroy", None, [_P]),
     ("bmc_cuda_rollout_device", C.c_int, [_P, C.POINTER(Terms), C.c_size_t, C.POINTER(World),
                                           C.POINTER(RunOpts), C.POINTER(Outputs), _P, _P]),
     ("bmc_cuda_last_kernel_ms", C.c_int, [_P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),

@@ -1,9 +1,8 @@
 // bmc_capi.cpp -- the C-ABI (include/brakemc_cuda.h): device contexts, the
-// actuator-table cache, the chunked host<->device pipeline behind
-// bmc_cuda_run, and the host composition of the statistics kernels.
+// actuator-table cache, rollout plans, and the chunked host<->device
+// pipeline behind bmc_cuda_run / bmc_cuda_run_model.
 //
-// Compiled by g++ with -ffp-contract=off: the double-double merges and the
-// final statistics formulas below must not be contracted into FMAs.
+// Compiled by g++ with -ffp-contract=off.
 #include "bmc_ctx.h"
 
 #include <algorithm>
@@ -18,7 +17,7 @@
 namespace bmc {
 namespace {
 
-constexpr size_t kTableCap = size_t{1} << 20;      // 32 MB of stage values
+constexpr size_t kTableCap = size_t{1} << 20;          // 32 MB of stage values
 constexpr uint64_t kDefaultChunk = uint64_t{1} << 22;  // 4M samples per pipeline slot
 constexpr int kMaxCoarseSteps = 2048;
 constexpr int kBucketsTarget = 2000;  // step buckets; x2 clamp classes <= 4096 keys
@@ -26,6 +25,16 @@ constexpr int kBucketsTarget = 2000;  // step buckets; x2 clamp classes <= 4096 
 bool same_key(const WorldDerived& a, const WorldDerived& b) {
     return std::memcmp(&a, &b, sizeof a) == 0;
 }
+
+int bucket_width(const WorldDerived& d) {
+    return static_cast<int>((d.max_steps + kBucketsTarget) / kBucketsTarget);
+}
+
+int bucket_count(const WorldDerived& d) {
+    return 2 * (static_cast<int>(d.max_steps / bucket_width(d)) + 1);
+}
+
+}  // namespace
 
 int ensure_table(bmc_ctx* ctx, const WorldDerived& d) {
     if (ctx->have_table && same_key(ctx->tkey, d)) return BMC_OK;
@@ -79,69 +88,91 @@ int ensure_table(bmc_ctx* ctx, const WorldDerived& d) {
     return BMC_OK;
 }
 
-// Enqueue predictor/binning (optional) + rollout for n samples on `s`.
-int enqueue_rollout(bmc_ctx* ctx, const bmc_terms& terms, uint64_t n, const WorldDerived& d,
-                    const bmc_run_opts& opts, const bmc_outputs& out,
-                    unsigned long long* total_steps_dev, cudaStream_t s, KernelEvents& ev,
-                    uint32_t* launches) {
-    if (n >= (uint64_t{1} << 32)) {
-        return fail(ctx, BMC_E_CONFIG, "batch: at most 2^32-1 samples per device launch");
-    }
-    int rc = ensure_table(ctx, d);
+int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uint64_t n,
+              Plan* plan) {
+    (void)n;
+    const int rc = ensure_table(ctx, d);
     if (rc != BMC_OK) return rc;
-
+    Plan p;
+    p.d = d;
     int mode = opts.table_mode;
     if (mode == kTableAuto) mode = ctx->t_len <= kSmemTableMax ? kTableShared : kTableGlobal;
     if (mode == kTableShared && ctx->t_len > kSmemTableMax) mode = kTableGlobal;
     if (!ctx->t_converged) mode = kTableNone;
-
     int sched = opts.schedule;
     if (sched == kScheduleDefault) sched = kScheduleBinned;
     if (ctx->coarse_len == 0 || mode == kTableNone) sched = kScheduleIndex;
-
     int bt = opts.block_threads;
     if (bt == 0) bt = mode == kTableGlobal ? 256 : 1024;
+    if (bt != 256 && bt != 512 && bt != 768 && bt != 1024) {
+        return fail(ctx, BMC_E_CONFIG, "execution.block_threads: must be 256, 512, 768 or 1024");
+    }
+    p.mode = mode;
+    p.sched = sched;
+    p.bt = bt;
+    p.table = ctx->d_table.as<StageA>();
+    p.table_len = ctx->t_len;
+    p.table_min = ctx->t_min;
+    p.coarse = ctx->d_coarse.as<float>();
+    p.coarse_len = ctx->coarse_len;
+    p.coarse_h = ctx->coarse_h;
+    *plan = p;
+    return BMC_OK;
+}
 
+int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n) {
+    // counter: [0] work counter (u32) | [8] executed steps | [16] lane slots
+    BMC_CK(ctx, sc.counter.reserve(64));
+    if (plan.sched == kScheduleBinned) {
+        BMC_CK(ctx, sc.keys.reserve(std::max<uint64_t>(n, 1) * sizeof(uint16_t)));
+        BMC_CK(ctx, sc.perm.reserve(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
+        BMC_CK(ctx, sc.hist.reserve(4096 * sizeof(unsigned int)));
+    }
+    return BMC_OK;
+}
+
+int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms& terms,
+                    uint64_t n, const bmc_outputs& out, unsigned long long* total_steps_dev,
+                    cudaStream_t s, KernelEvents* ev, uint32_t* launches) {
+    if (n >= (uint64_t{1} << 32)) {
+        return fail(ctx, BMC_E_CONFIG, "batch: at most 2^32-1 samples per device launch");
+    }
+    int rc = reserve_scratch(ctx, sc, plan, n);
+    if (rc != BMC_OK) return rc;
+    const WorldDerived& d = plan.d;
     uint32_t nl = 0;
     const uint32_t* perm = nullptr;
-    ev.predicted = false;
-    if (sched == kScheduleBinned && n > 0) {
-        const int width = static_cast<int>((d.max_steps + kBucketsTarget) / kBucketsTarget);
-        const int buckets = 2 * (static_cast<int>(d.max_steps / width) + 1);
-        BMC_CK(ctx, ctx->keys.reserve(n * sizeof(uint16_t)));
-        BMC_CK(ctx, ctx->perm.reserve(n * sizeof(uint32_t)));
-        BMC_CK(ctx, ctx->hist.reserve(4096 * sizeof(unsigned int)));
-        BMC_CK(ctx, cudaEventRecord(ev.p0, s));
-        BMC_CK(ctx, cudaMemsetAsync(ctx->hist.p, 0, buckets * sizeof(unsigned int), s));
+    if (ev) ev->predicted = false;
+    if (plan.sched == kScheduleBinned && n > 0) {
+        const int buckets = bucket_count(d);
+        if (ev) BMC_CK(ctx, cudaEventRecord(ev->p0, s));
+        BMC_CK(ctx, cudaMemsetAsync(sc.hist.p, 0, buckets * sizeof(unsigned int), s));
         PredictArgs pa{};
         pa.v0 = terms.initial_speed;
         pa.brake_floor = terms.brake_floor;
         pa.drag = terms.drag_factor;
         pa.grade = terms.grade_accel;
         pa.n = n;
-        pa.coarse_a = ctx->d_coarse.as<float>();
-        pa.coarse_len = ctx->coarse_len;
-        pa.h = ctx->coarse_h;
+        pa.coarse_a = plan.coarse;
+        pa.coarse_len = plan.coarse_len;
+        pa.h = plan.coarse_h;
         pa.inv_dt = static_cast<float>(1.0 / d.dt);
         pa.max_steps = static_cast<int32_t>(d.max_steps);
-        pa.bucket_width = width;
+        pa.bucket_width = bucket_width(d);
         pa.buckets = buckets;
-        pa.table_min = ctx->t_min;
-        pa.keys = ctx->keys.as<uint16_t>();
-        pa.hist = ctx->hist.as<unsigned int>();
+        pa.table_min = plan.table_min;
+        pa.keys = sc.keys.as<uint16_t>();
+        pa.hist = sc.hist.as<unsigned int>();
         BMC_CK(ctx, launch_predict(pa, s));
-        BMC_CK(ctx, launch_bin_scan(ctx->hist.as<unsigned int>(), buckets, s));
-        BMC_CK(ctx, launch_bin_scatter(ctx->keys.as<uint16_t>(), n, ctx->hist.as<unsigned int>(),
-                                       ctx->perm.as<uint32_t>(), s));
-        BMC_CK(ctx, cudaEventRecord(ev.p1, s));
+        BMC_CK(ctx, launch_bin_scan(sc.hist.as<unsigned int>(), buckets, s));
+        BMC_CK(ctx, launch_bin_scatter(sc.keys.as<uint16_t>(), n, sc.hist.as<unsigned int>(),
+                                       sc.perm.as<uint32_t>(), s));
+        if (ev) BMC_CK(ctx, cudaEventRecord(ev->p1, s));
         nl += 3;
-        perm = ctx->perm.as<uint32_t>();
-        ev.predicted = true;
+        perm = sc.perm.as<uint32_t>();
+        if (ev) ev->predicted = true;
     }
-
-    // [0] work counter (u32) | [8] executed steps (u64) | [16] lane slots (u64)
-    BMC_CK(ctx, ctx->counter.reserve(64));
-    BMC_CK(ctx, cudaMemsetAsync(ctx->counter.p, 0, 24, s));
+    BMC_CK(ctx, cudaMemsetAsync(sc.counter.p, 0, 24, s));
     RolloutArgs ra{};
     ra.v0 = terms.initial_speed;
     ra.brake_floor = terms.brake_floor;
@@ -155,21 +186,174 @@ int enqueue_rollout(bmc_ctx* ctx, const bmc_terms& terms, uint64_t n, const Worl
     ra.brake_cmd = d.brake_cmd;
     ra.inv_tau = d.inv_tau;
     ra.max_steps = static_cast<int32_t>(d.max_steps);
-    ra.table = ctx->d_table.as<StageA>();
-    ra.table_len = ctx->t_len;
+    ra.table = plan.table;
+    ra.table_len = plan.table_len;
     ra.stop_distance = out.stop_distance;
     ra.steps = out.steps;
     ra.hit_horizon = out.hit_horizon;
     ra.total_steps = total_steps_dev;
-    ra.work_counter = ctx->counter.as<unsigned int>();
-    ra.counters = reinterpret_cast<unsigned long long*>(ctx->counter.as<char>() + 8);
-    BMC_CK(ctx, cudaEventRecord(ev.r0, s));
+    ra.work_counter = sc.counter.as<unsigned int>();
+    ra.counters = reinterpret_cast<unsigned long long*>(sc.counter.as<char>() + 8);
+    if (ev) BMC_CK(ctx, cudaEventRecord(ev->r0, s));
     if (n > 0) {
-        BMC_CK(ctx, launch_rollout(ra, mode, bt, s));
+        BMC_CK(ctx, launch_rollout(ra, plan.mode, plan.bt, s));
         ++nl;
     }
-    BMC_CK(ctx, cudaEventRecord(ev.r1, s));
+    if (ev) BMC_CK(ctx, cudaEventRecord(ev->r1, s));
     if (launches) *launches += nl;
+    return BMC_OK;
+}
+
+namespace {
+
+// Chunked host<->device pipeline (2 slots): per chunk the host pool fills
+// pinned SoA terms (from AoS samples, or straight from the sampler), the
+// h2d stream copies them, the compute stream bins + rolls out, and either
+// the d2h stream returns the compact outputs for the host unpack, or the
+// kernel writes straight into caller-owned device outputs.
+int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const bmc_run_opts& o,
+                 uint64_t n, const bmc_sample* samples, const bmc_model* model, uint64_t first,
+                 bmc_result* host_out, const bmc_outputs* dev_out, bmc_run_info* info,
+                 uint64_t* clamp_count) {
+    using Clock = std::chrono::steady_clock;
+    const uint64_t chunk = std::min<uint64_t>(o.chunk_samples ? o.chunk_samples : kDefaultChunk, n);
+    const unsigned threads = resolve_threads(o.host_threads);
+    Plan plan;
+    int rc = make_plan(ctx, d, o, chunk, &plan);
+    if (rc != BMC_OK) return rc;
+    for (auto& s : ctx->slots) {
+        BMC_CK(ctx, s.h_terms.reserve(chunk * 32));
+        BMC_CK(ctx, s.d_terms.reserve(chunk * 32));
+        if (host_out) {
+            BMC_CK(ctx, s.h_out.reserve(chunk * 13));
+            BMC_CK(ctx, s.d_out.reserve(chunk * 13));
+        }
+        s.busy = false;
+    }
+    BMC_CK(ctx, ctx->total_steps.reserve(sizeof(unsigned long long)));
+    BMC_CK(ctx, cudaMemsetAsync(ctx->total_steps.p, 0, sizeof(unsigned long long), ctx->stream));
+    rc = reserve_scratch(ctx, ctx->scratch, plan, chunk);
+    if (rc != BMC_OK) return rc;
+
+    double kernel_ms = 0.0, predict_ms = 0.0;
+    uint32_t launches = 0;
+    std::atomic<uint64_t> clamps{0};
+    const auto t0 = Clock::now();
+
+    auto finish = [&](Slot& s) -> int {
+        if (!s.busy) return BMC_OK;
+        BMC_CK(ctx, cudaEventSynchronize(s.d2h_done));
+        float ms = 0.0f;
+        BMC_CK(ctx, cudaEventElapsedTime(&ms, s.kev.r0, s.kev.r1));
+        kernel_ms += ms;
+        if (s.kev.predicted) {
+            BMC_CK(ctx, cudaEventElapsedTime(&ms, s.kev.p0, s.kev.p1));
+            predict_ms += ms;
+        }
+        if (host_out) {
+            const double* dd = s.h_out.as<double>();
+            const int32_t* st = reinterpret_cast<const int32_t*>(s.h_out.as<char>() + s.len * 8);
+            const uint8_t* hz = reinterpret_cast<const uint8_t*>(s.h_out.as<char>() + s.len * 12);
+            bmc_result* dst = host_out + s.offset;
+            const double dt = d.dt;
+            host_pool().parallel_for(
+                s.len,
+                [&](size_t b, size_t e) {
+                    for (size_t i = b; i < e; ++i) {
+                        bmc_result r;
+                        std::memset(&r, 0, sizeof r);
+                        r.stop_distance = dd[i];
+                        r.stop_time = static_cast<double>(st[i]) * dt;  // integrator.cpp:23,27
+                        r.steps = st[i];
+                        r.hit_horizon = hz[i];
+                        dst[i] = r;
+                    }
+                },
+                threads);
+        }
+        s.busy = false;
+        return BMC_OK;
+    };
+
+    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    for (uint64_t k = 0; k < nchunks; ++k) {
+        Slot& s = ctx->slots[k & 1];
+        if ((rc = finish(s)) != BMC_OK) return rc;
+        s.offset = k * chunk;
+        s.len = std::min<uint64_t>(chunk, n - s.offset);
+        double* hv0 = s.h_terms.as<double>();
+        double* hfl = hv0 + s.len;
+        double* hdr = hfl + s.len;
+        double* hgr = hdr + s.len;
+        std::atomic<int> status{BMC_OK};
+        host_pool().parallel_for(
+            s.len,
+            [&](size_t b, size_t e) {
+                int r;
+                if (samples) {
+                    r = stage_terms_serial(samples + s.offset + b, e - b, w, hv0 + b, hfl + b,
+                                           hdr + b, hgr + b);
+                } else {
+                    uint64_t c = 0;
+                    r = draw_terms_serial(*model, first + s.offset + b, e - b, w, hv0 + b, hfl + b,
+                                          hdr + b, hgr + b, &c);
+                    clamps += c;
+                }
+                if (r != BMC_OK) status = r;
+            },
+            threads);
+        if (status != BMC_OK) {
+            cudaStreamSynchronize(ctx->stream);
+            cudaStreamSynchronize(ctx->d2h);
+            return fail(ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
+        }
+        BMC_CK(ctx, cudaMemcpyAsync(s.d_terms.p, s.h_terms.p, s.len * 32, cudaMemcpyHostToDevice, ctx->h2d));
+        BMC_CK(ctx, cudaEventRecord(s.h2d_done, ctx->h2d));
+        BMC_CK(ctx, cudaStreamWaitEvent(ctx->stream, s.h2d_done, 0));
+        const double* dv0 = s.d_terms.as<double>();
+        const bmc_terms terms{dv0, dv0 + s.len, dv0 + 2 * s.len, dv0 + 3 * s.len};
+        bmc_outputs outs;
+        if (host_out) {
+            char* dout = s.d_out.as<char>();
+            outs = bmc_outputs{reinterpret_cast<double*>(dout),
+                               reinterpret_cast<int32_t*>(dout + s.len * 8),
+                               reinterpret_cast<uint8_t*>(dout + s.len * 12)};
+        } else {
+            outs = bmc_outputs{dev_out->stop_distance ? dev_out->stop_distance + s.offset : nullptr,
+                               dev_out->steps ? dev_out->steps + s.offset : nullptr,
+                               dev_out->hit_horizon ? dev_out->hit_horizon + s.offset : nullptr};
+        }
+        rc = enqueue_rollout(ctx, plan, ctx->scratch, terms, s.len, outs,
+                             ctx->total_steps.as<unsigned long long>(), ctx->stream, &s.kev,
+                             &launches);
+        if (rc != BMC_OK) return rc;
+        BMC_CK(ctx, cudaEventRecord(s.compute_done, ctx->stream));
+        BMC_CK(ctx, cudaStreamWaitEvent(ctx->d2h, s.compute_done, 0));
+        if (host_out) {
+            // d_out holds d (8B), steps (4B), horizon (1B) blocks contiguously
+            BMC_CK(ctx, cudaMemcpyAsync(s.h_out.p, s.d_out.p, s.len * 13, cudaMemcpyDeviceToHost, ctx->d2h));
+        }
+        BMC_CK(ctx, cudaEventRecord(s.d2h_done, ctx->d2h));
+        s.busy = true;
+    }
+    for (uint64_t k = nchunks > 2 ? nchunks - 2 : 0; k < nchunks; ++k) {
+        if ((rc = finish(ctx->slots[k & 1])) != BMC_OK) return rc;
+    }
+    unsigned long long steps_total = 0;
+    BMC_CK(ctx, cudaMemcpy(&steps_total, ctx->total_steps.p, sizeof steps_total, cudaMemcpyDeviceToHost));
+    const double wall = std::chrono::duration<double>(Clock::now() - t0).count();
+    ctx->last_launches = launches;
+    if (clamp_count) *clamp_count = clamps.load();
+    if (info) {
+        info->wall_s = wall;
+        info->kernel_ms = kernel_ms;
+        info->predict_ms = predict_ms;
+        info->total_steps = steps_total;
+        info->h2d_bytes = n * 32;
+        info->d2h_bytes = host_out ? n * 13 : 0;
+        info->launches = launches;
+        info->chunks = static_cast<uint32_t>(nchunks);
+    }
     return BMC_OK;
 }
 
@@ -248,12 +432,12 @@ void bmc_cuda_destroy(bmc_ctx* ctx) {
         if (s.d2h_done) cudaEventDestroy(s.d2h_done);
         s.kev.destroy();
     }
-    for (bmc::DevBuf* b : {&ctx->d_table, &ctx->d_coarse, &ctx->keys, &ctx->perm, &ctx->hist,
-                           &ctx->counter, &ctx->total_steps, &ctx->partials, &ctx->sel_hist,
-                           &ctx->sel_pref, &ctx->sorted_h, &ctx->buckets, &ctx->hist_buf}) {
+    for (bmc::DevBuf* b : {&ctx->d_table, &ctx->d_coarse, &ctx->total_steps, &ctx->partials,
+                           &ctx->sel_hist, &ctx->sel_pref, &ctx->sorted_h, &ctx->buckets,
+                           &ctx->hist_buf}) {
         b->release();
     }
-    ctx->h_small.release();
+    ctx->scratch.release();
     ctx->kev.destroy();
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
@@ -285,10 +469,11 @@ int bmc_cuda_rollout_device(bmc_ctx* ctx, const bmc_terms* terms, size_t n, cons
     if ((rc = bmc::derive_world(*world, &d, &err)) != BMC_OK) return fail(ctx, rc, err);
     const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    bmc::Plan plan;
+    if ((rc = bmc::make_plan(ctx, d, o, n, &plan)) != BMC_OK) return rc;
     ctx->last_launches = 0;
-    rc = bmc::enqueue_rollout(ctx, *terms, n, d, o, *out, total_steps_dev, s, ctx->kev,
-                              &ctx->last_launches);
-    return rc;
+    return bmc::enqueue_rollout(ctx, plan, ctx->scratch, *terms, n, *out, total_steps_dev, s,
+                                &ctx->kev, &ctx->last_launches);
 }
 
 int bmc_cuda_last_kernel_ms(bmc_ctx* ctx, float* rollout_ms, float* predict_ms) {
@@ -302,16 +487,29 @@ int bmc_cuda_last_kernel_ms(bmc_ctx* ctx, float* rollout_ms, float* predict_ms) 
     return BMC_OK;
 }
 
+int bmc_cuda_last_lane_stats(bmc_ctx* ctx, uint64_t* steps, uint64_t* slots) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    unsigned long long c[2] = {0, 0};
+    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->scratch.counter.p) {
+        BMC_CK(ctx, cudaMemcpy(c, ctx->scratch.counter.as<char>() + 8, sizeof c, cudaMemcpyDeviceToHost));
+    }
+    if (steps) *steps = c[0];
+    if (slots) *slots = c[1];
+    return BMC_OK;
+}
+
 int bmc_cuda_fp64_peak(bmc_ctx* ctx, int reps, double* ops_per_s, double* best_ms) {
     int rc = bmc::prepare(ctx);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(ctx->mu);
-    BMC_CK(ctx, ctx->counter.reserve(64));
+    BMC_CK(ctx, ctx->scratch.counter.reserve(64));
     double best = 1e30;
     uint64_t ops = 0;
     for (int r = 0; r < std::max(1, reps) + 1; ++r) {  // first launch is a warm-up
         BMC_CK(ctx, cudaEventRecord(ctx->kev.r0, ctx->stream));
-        BMC_CK(ctx, bmc::launch_fp64_probe(ctx->counter.as<double>(), 4096, &ops, ctx->stream));
+        BMC_CK(ctx, bmc::launch_fp64_probe(ctx->scratch.counter.as<double>(), 4096, &ops, ctx->stream));
         BMC_CK(ctx, cudaEventRecord(ctx->kev.r1, ctx->stream));
         BMC_CK(ctx, cudaEventSynchronize(ctx->kev.r1));
         float ms = 0.0f;
@@ -323,19 +521,6 @@ int bmc_cuda_fp64_peak(bmc_ctx* ctx, int reps, double* ops_per_s, double* best_m
     return BMC_OK;
 }
 
-int bmc_cuda_last_lane_stats(bmc_ctx* ctx, uint64_t* steps, uint64_t* slots) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    unsigned long long c[2] = {0, 0};
-    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
-    if (ctx->counter.p) {
-        BMC_CK(ctx, cudaMemcpy(c, ctx->counter.as<char>() + 8, sizeof c, cudaMemcpyDeviceToHost));
-    }
-    if (steps) *steps = c[0];
-    if (slots) *slots = c[1];
-    return BMC_OK;
-}
-
 int bmc_cuda_last_launches(bmc_ctx* ctx, uint32_t* launches) {
     if (!ctx || !launches) return BMC_E_CONFIG;
     *launches = ctx->last_launches;
@@ -344,7 +529,6 @@ int bmc_cuda_last_launches(bmc_ctx* ctx, uint32_t* launches) {
 
 int bmc_cuda_run(bmc_ctx* ctx, const bmc_sample* samples, size_t n, const bmc_world* world,
                  const bmc_run_opts* opts, bmc_result* out, bmc_run_info* info) {
-    using Clock = std::chrono::steady_clock;
     int rc = bmc::prepare(ctx);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -354,118 +538,26 @@ int bmc_cuda_run(bmc_ctx* ctx, const bmc_sample* samples, size_t n, const bmc_wo
     std::string err;
     if ((rc = bmc::derive_world(*world, &d, &err)) != BMC_OK) return fail(ctx, rc, err);
     const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
-    const uint64_t chunk = std::min<uint64_t>(o.chunk_samples ? o.chunk_samples : bmc::kDefaultChunk, n);
-    const unsigned threads = bmc::resolve_threads(o.host_threads);
+    return bmc::run_pipeline(ctx, *world, d, o, n, samples, nullptr, 0, out, nullptr, info, nullptr);
+}
 
-    for (auto& s : ctx->slots) {
-        BMC_CK(ctx, s.h_terms.reserve(chunk * 32));
-        BMC_CK(ctx, s.h_out.reserve(chunk * 13));
-        BMC_CK(ctx, s.d_terms.reserve(chunk * 32));
-        BMC_CK(ctx, s.d_out.reserve(chunk * 13));
-        s.busy = false;
+int bmc_cuda_run_model(bmc_ctx* ctx, const bmc_model* model, uint64_t first, size_t n,
+                       const bmc_world* world, const bmc_run_opts* opts, bmc_result* host_out,
+                       const bmc_outputs* dev_out, uint64_t* clamp_count, bmc_run_info* info) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (n == 0) return fail(ctx, BMC_E_CONFIG, "samples: must be >= 1");  // sampling.cpp:68-70
+    if (!model || !world) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_run_model: null argument");
+    if ((host_out == nullptr) == (dev_out == nullptr)) {
+        return fail(ctx, BMC_E_CONFIG, "bmc_cuda_run_model: exactly one of host_out / dev_out");
     }
-    BMC_CK(ctx, ctx->total_steps.reserve(sizeof(unsigned long long)));
-    BMC_CK(ctx, cudaMemsetAsync(ctx->total_steps.p, 0, sizeof(unsigned long long), ctx->stream));
-
-    double kernel_ms = 0.0, predict_ms = 0.0;
-    uint32_t launches = 0;
-    const auto t0 = Clock::now();
-
-    auto finish = [&](bmc::Slot& s) -> int {
-        if (!s.busy) return BMC_OK;
-        BMC_CK(ctx, cudaEventSynchronize(s.d2h_done));
-        float ms = 0.0f;
-        BMC_CK(ctx, cudaEventElapsedTime(&ms, s.kev.r0, s.kev.r1));
-        kernel_ms += ms;
-        if (s.kev.predicted) {
-            BMC_CK(ctx, cudaEventElapsedTime(&ms, s.kev.p0, s.kev.p1));
-            predict_ms += ms;
-        }
-        const double* dd = s.h_out.as<double>();
-        const int32_t* st = reinterpret_cast<const int32_t*>(s.h_out.as<char>() + s.len * 8);
-        const uint8_t* hz = reinterpret_cast<const uint8_t*>(s.h_out.as<char>() + s.len * 12);
-        bmc_result* dst = out + s.offset;
-        const double dt = d.dt;
-        bmc::host_pool().parallel_for(
-            s.len,
-            [&](size_t b, size_t e) {
-                for (size_t i = b; i < e; ++i) {
-                    bmc_result r;
-                    std::memset(&r, 0, sizeof r);
-                    r.stop_distance = dd[i];
-                    r.stop_time = static_cast<double>(st[i]) * dt;  // integrator.cpp:23,27
-                    r.steps = st[i];
-                    r.hit_horizon = hz[i];
-                    dst[i] = r;
-                }
-            },
-            threads);
-        s.busy = false;
-        return BMC_OK;
-    };
-
-    const uint64_t nchunks = (n + chunk - 1) / chunk;
-    for (uint64_t k = 0; k < nchunks; ++k) {
-        bmc::Slot& s = ctx->slots[k & 1];
-        if ((rc = finish(s)) != BMC_OK) return rc;
-        s.offset = k * chunk;
-        s.len = std::min<uint64_t>(chunk, n - s.offset);
-        double* hv0 = s.h_terms.as<double>();
-        double* hfl = hv0 + s.len;
-        double* hdr = hfl + s.len;
-        double* hgr = hdr + s.len;
-        std::atomic<int> status{BMC_OK};
-        bmc::host_pool().parallel_for(
-            s.len,
-            [&](size_t b, size_t e) {
-                const int r = bmc::stage_terms_serial(samples + s.offset + b, e - b, *world, hv0 + b,
-                                                      hfl + b, hdr + b, hgr + b);
-                if (r != BMC_OK) status = r;
-            },
-            threads);
-        if (status != BMC_OK) {
-            cudaStreamSynchronize(ctx->stream);
-            cudaStreamSynchronize(ctx->d2h);
-            return fail(ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
-        }
-        BMC_CK(ctx, cudaMemcpyAsync(s.d_terms.p, s.h_terms.p, s.len * 32, cudaMemcpyHostToDevice, ctx->h2d));
-        BMC_CK(ctx, cudaEventRecord(s.h2d_done, ctx->h2d));
-        BMC_CK(ctx, cudaStreamWaitEvent(ctx->stream, s.h2d_done, 0));
-        const double* dv0 = s.d_terms.as<double>();
-        bmc_terms terms{dv0, dv0 + s.len, dv0 + 2 * s.len, dv0 + 3 * s.len};
-        char* dout = s.d_out.as<char>();
-        bmc_outputs outs{reinterpret_cast<double*>(dout), reinterpret_cast<int32_t*>(dout + s.len * 8),
-                         reinterpret_cast<uint8_t*>(dout + s.len * 12)};
-        rc = bmc::enqueue_rollout(ctx, terms, s.len, d, o, outs,
-                                  ctx->total_steps.as<unsigned long long>(), ctx->stream, s.kev,
-                                  &launches);
-        if (rc != BMC_OK) return rc;
-        BMC_CK(ctx, cudaEventRecord(s.compute_done, ctx->stream));
-        BMC_CK(ctx, cudaStreamWaitEvent(ctx->d2h, s.compute_done, 0));
-        // d_out holds d (8B), steps (4B), horizon (1B) blocks contiguously
-        BMC_CK(ctx, cudaMemcpyAsync(s.h_out.p, s.d_out.p, s.len * 13, cudaMemcpyDeviceToHost, ctx->d2h));
-        BMC_CK(ctx, cudaEventRecord(s.d2h_done, ctx->d2h));
-        s.busy = true;
-    }
-    // drain in submission order
-    for (uint64_t k = nchunks > 2 ? nchunks - 2 : 0; k < nchunks; ++k) {
-        if ((rc = finish(ctx->slots[k & 1])) != BMC_OK) return rc;
-    }
-    unsigned long long steps_total = 0;
-    BMC_CK(ctx, cudaMemcpy(&steps_total, ctx->total_steps.p, sizeof steps_total, cudaMemcpyDeviceToHost));
-    const double wall = std::chrono::duration<double>(Clock::now() - t0).count();
-    ctx->last_launches = launches;
-    if (info) {
-        info->wall_s = wall;
-        info->kernel_ms = kernel_ms;
-        info->predict_ms = predict_ms;
-        info->total_steps = steps_total;
-        info->h2d_bytes = static_cast<uint64_t>(n) * 32;
-        info->d2h_bytes = static_cast<uint64_t>(n) * 13;
-        info->launches = launches;
-        info->chunks = static_cast<uint32_t>(nchunks);
-    }
-    return BMC_OK;
+    bmc::WorldDerived d{};
+    std::string err;
+    if ((rc = bmc::derive_world(*world, &d, &err)) != BMC_OK) return fail(ctx, rc, err);
+    const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
+    return bmc::run_pipeline(ctx, *world, d, o, n, nullptr, model, first, host_out, dev_out, info,
+                             clamp_count);
 }
 
 }  // extern "C"

@@ -1,5 +1,6 @@
 // bmc_ctx.h -- the device context behind the opaque bmc_ctx handle, shared
-// by the C-ABI translation units (bmc_capi.cpp, bmc_capi_stats.cpp).
+// by the C-ABI translation units (bmc_capi.cpp, bmc_capi_stats.cpp,
+// bmc_graph.cpp).
 #pragma once
 
 #include "bmc_kernels.h"
@@ -73,6 +74,34 @@ struct KernelEvents {
     }
 };
 
+// Device buffers one rollout launch needs besides its inputs/outputs.
+// A CUDA graph owns its own Scratch so captured pointers stay valid.
+struct Scratch {
+    DevBuf keys, perm, hist, counter;
+    void release() {
+        keys.release();
+        perm.release();
+        hist.release();
+        counter.release();
+    }
+};
+
+// Everything a rollout launch needs that depends on the world, not on the
+// samples: the actuator table, the predictor's coarse table and the chosen
+// kernel variant.  Pointers refer to ctx-owned (or graph-owned) buffers.
+struct Plan {
+    WorldDerived d{};
+    int mode = kTableNone;
+    int sched = kScheduleIndex;
+    int bt = 1024;
+    const StageA* table = nullptr;
+    int table_len = 0;
+    double table_min = 0.0;
+    const float* coarse = nullptr;
+    int coarse_len = 0;
+    float coarse_h = 0.0f;
+};
+
 struct Slot {
     PinBuf h_terms, h_out;
     DevBuf d_terms, d_out;
@@ -101,15 +130,13 @@ struct bmc_ctx {
     int coarse_len = 0;
     float coarse_h = 0.0f;
 
-    bmc::DevBuf keys, perm, hist, counter, total_steps;
+    bmc::Scratch scratch;
+    bmc::DevBuf total_steps;
     uint32_t last_launches = 0;
-    float last_roll_ms = 0.0f, last_pred_ms = 0.0f;
 
     bmc::Slot slots[2];
     bmc::DevBuf partials, sel_hist, sel_pref, sorted_h, buckets, hist_buf;
-    bmc::PinBuf h_small;
 };
-
 
 namespace bmc {
 
@@ -136,5 +163,15 @@ inline int prepare(bmc_ctx* ctx) {
     return BMC_OK;
 }
 
+// bmc_capi.cpp
+int ensure_table(bmc_ctx* ctx, const WorldDerived& d);
+int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uint64_t n,
+              Plan* plan);
+int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n);
+// Enqueue predictor/binning (when planned) + rollout on `s`.  ev may be
+// null (no timing events, e.g. under stream capture).
+int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms& terms,
+                    uint64_t n, const bmc_outputs& out, unsigned long long* total_steps_dev,
+                    cudaStream_t s, KernelEvents* ev, uint32_t* launches);
 
 }  // namespace bmc

@@ -161,6 +161,24 @@ int stage_terms_serial(const bmc_sample* s, std::size_t n, const bmc_world& w, d
     return BMC_OK;
 }
 
+int draw_terms_serial(const bmc_model& m, uint64_t first, std::size_t n, const bmc_world& w,
+                      double* v0, double* floor, double* drag, double* grade, uint64_t* clamps) {
+    // draw_batch (sampling.cpp:67-100) fused with RolloutTerms::from
+    // (dynamics.cpp:57-68): no AoS sample is materialised, each sample goes
+    // straight into the pinned SoA staging buffers.
+    constexpr std::size_t kBlock = 256;
+    bmc_sample tmp[kBlock];
+    uint64_t c = 0;
+    for (std::size_t b = 0; b < n; b += kBlock) {
+        const std::size_t k = std::min(kBlock, n - b);
+        c += draw_range_serial(m, first + b, k, tmp);
+        const int rc = stage_terms_serial(tmp, k, w, v0 + b, floor + b, drag + b, grade + b);
+        if (rc != BMC_OK) return rc;
+    }
+    if (clamps) *clamps += c;
+    return BMC_OK;
+}
+
 // ------------------------------------------------------------ thread pool
 
 ThreadPool::ThreadPool(unsigned threads) {

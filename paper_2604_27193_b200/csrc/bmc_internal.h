@@ -76,6 +76,8 @@ unsigned resolve_threads(int requested);
 uint64_t draw_range_serial(const bmc_model& m, uint64_t first, std::size_t n, bmc_sample* out);
 int stage_terms_serial(const bmc_sample* s, std::size_t n, const bmc_world& w, double* v0,
                        double* floor, double* drag, double* grade);
+int draw_terms_serial(const bmc_model& m, uint64_t first, std::size_t n, const bmc_world& w,
+                      double* v0, double* floor, double* drag, double* grade, uint64_t* clamps);
 
 void set_error(const std::string& msg);
 const std::string& get_error();

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
     if (MODE == kTableShared) {
         const double2* src = reinterpret_cast<const double2*>(A.table);
         double2* dst = reinterpret_cast<double2*>(smem_raw);
-        for (int i = threadIdx.x; i < 2 * len; i += BT) dst[i] = src[i];
+        for (int i = threadIdx.x; i < 2 * len; i += blockDim.x) dst[i] = src[i];
         __syncthreads();
         tab = reinterpret_cast<const StageA*>(smem_raw);
     }
@@ -375,11 +375,20 @@ cudaError_t launch_rollout_t(const RolloutArgs& a, cudaStream_t s) {
                                                                   BT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    // Persistent grid.  Small batches (the real-time case) spread their
+    // 32-sample groups over every SM with narrower CTAs instead of packing
+    // them into a few full ones: fewer warps per SM = shorter per-step
+    // latency of each dependent RK4 chain.
     const uint64_t groups = (a.n + 31) / 32;
-    const uint64_t need = (groups + BT / 32 - 1) / (BT / 32);
-    const uint64_t resident = static_cast<uint64_t>(per_sm) * static_cast<uint64_t>(sm_count_cached(dev));
+    const uint64_t sms = static_cast<uint64_t>(sm_count_cached(dev));
+    const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+    uint64_t warps_per_block = BT / 32;
+    if (groups < resident * warps_per_block) {
+        warps_per_block = std::max<uint64_t>(1, (groups + resident - 1) / resident);
+    }
+    const uint64_t need = (groups + warps_per_block - 1) / warps_per_block;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(need, resident)));
-    rollout_kernel<MODE, BT><<<grid, BT, smem, s>>>(a);
+    rollout_kernel<MODE, BT><<<grid, static_cast<int>(warps_per_block * 32), smem, s>>>(a);
     return cudaGetLastError();
 }
 

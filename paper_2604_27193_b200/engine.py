@@ -171,6 +171,41 @@ class CudaExecutor:
                          int(info.total_steps), int(info.h2d_bytes), int(info.d2h_bytes),
                          int(info.launches), int(info.chunks))
 
+    def run_model(self, model: UncertaintyModel, n: int, first: int = 0,
+                  world: SimWorld = SimWorld(), out: np.ndarray = None, device_out=None,
+                  **opts):
+        """Streaming executor: draw samples [first, first+n) of ``model`` on the
+        host pool straight into pinned SoA terms, overlapped with the GPU.
+        Results go to a host AoS array (``out``/default) or, when
+        ``device_out=(d f64, steps i32, hz u8)`` CUDA tensors are given, stay on
+        the device (stats-only mode).  Returns (RunReport, clamp_count)."""
+        w = world.c()
+        o = self._opts(**opts)
+        info = N.RunInfo()
+        clamps = C.c_uint64(0)
+        m = model.c()
+        if device_out is not None:
+            outs = N.Outputs(*[int(x.data_ptr()) if x is not None else None for x in device_out])
+            self._check(self.lib.bmc_cuda_run_model(self.ctx, C.byref(m), first, n, C.byref(w),
+                                                    C.byref(o), None, C.byref(outs),
+                                                    C.byref(clamps), C.byref(info)))
+            res = None
+        else:
+            if out is None:
+                out = np.empty(n, dtype=RESULT_DTYPE)
+            self._check(self.lib.bmc_cuda_run_model(self.ctx, C.byref(m), first, n, C.byref(w),
+                                                    C.byref(o), _p(out), None, C.byref(clamps),
+                                                    C.byref(info)))
+            res = out
+        rep = RunReport(res, info.wall_s, "cuda", 1, info.kernel_ms, info.predict_ms,
+                        int(info.total_steps), int(info.h2d_bytes), int(info.d2h_bytes),
+                        int(info.launches), int(info.chunks))
+        return rep, int(clamps.value)
+
+    def graph(self, n: int, world: SimWorld = SimWorld(), **opts) -> "DecisionGraph":
+        """Capture the real-time decision batch of size n as a CUDA graph."""
+        return DecisionGraph(self, n, world, **opts)
+
     def rollout_device(self, terms, outputs, world: SimWorld = SimWorld(), total_steps=None,
                        stream=None, **opts) -> None:
         """Device-resident rollout. terms: 4 float64 CUDA tensors (v0, floor,
@@ -288,6 +323,110 @@ class CudaExecutor:
         heads = self.min_safe_headways(d, hz, levels)
         thr = [(r, h, ttc_for_headway(h, closing_speed)) for r, h in zip(levels, heads)]
         return probs, thr
+
+
+class DecisionGraph:
+    """Real-time mode (C2): fixed-size decision batch replayed as a CUDA graph."""
+
+    def __init__(self, ex: CudaExecutor, n: int, world: SimWorld = SimWorld(), **opts):
+        self.ex = ex
+        self.n = n
+        w = world.c()
+        o = ex._opts(**opts)
+        h = C.c_void_p()
+        ex._check(ex.lib.bmc_cuda_graph_create(ex.ctx, n, C.byref(w), C.byref(o), C.byref(h)))
+        self.g = h
+        self.out = np.empty(n, dtype=RESULT_DTYPE)
+
+    def run(self, samples: np.ndarray) -> RunReport:
+        samples = np.ascontiguousarray(samples, dtype=SAMPLE_DTYPE)
+        if samples.shape[0] != self.n:
+            raise N.ConfigError(f"batch: graph captured for {self.n} samples")
+        info = N.RunInfo()
+        self.ex._check(self.ex.lib.bmc_cuda_graph_run(self.g, _p(samples), _p(self.out),
+                                                      C.byref(info)))
+        return RunReport(self.out, info.wall_s, "cuda-graph", 1, total_steps=int(info.total_steps),
+                         h2d_bytes=int(info.h2d_bytes), d2h_bytes=int(info.d2h_bytes),
+                         launches=int(info.launches), chunks=1)
+
+    def run_model(self, model: UncertaintyModel, first: int = 0) -> RunReport:
+        info = N.RunInfo()
+        clamps = C.c_uint64(0)
+        m = model.c()
+        self.ex._check(self.ex.lib.bmc_cuda_graph_run_model(self.g, C.byref(m), first,
+                                                            _p(self.out), C.byref(clamps),
+                                                            C.byref(info)))
+        return RunReport(self.out, info.wall_s, "cuda-graph", 1, total_steps=int(info.total_steps),
+                         h2d_bytes=int(info.h2d_bytes), d2h_bytes=int(info.d2h_bytes),
+                         launches=int(info.launches), chunks=1)
+
+    def close(self):
+        if self.g:
+            self.ex.lib.bmc_cuda_graph_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def max_feasible_n(timed_run_s, budget_s: float, search_start: int, search_cap: int):
+    """Doubling + bisection search (analysis.cpp:258-318, same control flow):
+    largest n with timed_run_s(n) <= budget_s.  Returns (n, capped)."""
+    if not budget_s > 0.0:
+        raise N.ConfigError("budget: must be > 0")
+    if search_start == 0 or search_cap == 0:
+        raise N.ConfigError("feasibility.search: start and cap must be >= 1")
+    probe = min(search_start, search_cap)
+    lo = hi = 0
+    if timed_run_s(probe) <= budget_s:
+        lo = probe
+        while lo < search_cap:
+            nxt = min(search_cap, lo * 2)
+            if timed_run_s(nxt) <= budget_s:
+                lo = nxt
+            else:
+                hi = nxt
+                break
+        if hi == 0:
+            return lo, True
+    else:
+        hi = probe
+        down = probe // 2
+        while down >= 1:
+            if timed_run_s(down) <= budget_s:
+                lo = down
+                break
+            hi = down
+            down //= 2
+        if lo == 0:
+            return 0, False
+    while hi - lo > max(1, lo // 64):
+        mid = lo + (hi - lo) // 2
+        if timed_run_s(mid) <= budget_s:
+            lo = mid
+        else:
+            hi = mid
+    return lo, False
+
+
+def median_wall_time_s(fn, reps: int = 5, warmup: int = 1) -> float:
+    """backends.cpp:161-181 -- median of reps after warm-up, monotonic clock."""
+    import time
+    if reps < 1:
+        raise N.ConfigError("timing.reps: must be >= 1")
+    for _ in range(warmup):
+        fn()
+    ts = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t)
+    ts.sort()
+    mid = len(ts) // 2
+    return ts[mid] if len(ts) % 2 else 0.5 * (ts[mid - 1] + ts[mid])
 
 
 def ttc_for_headway(headway_m: float, closing_speed_mps: float) -> float:

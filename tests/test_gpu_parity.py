@@ -164,3 +164,67 @@ def test_cpp_executor_api():
     p = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     print(p.stdout)
     assert p.returncode == 0, p.stdout + p.stderr
+
+
+# ------------------------------------------------ streaming / real-time modes
+
+@pytest.mark.parametrize("first,n", [(0, 20000), (123457, 9001)])
+def test_run_model_matches_reference(ref, executor, first, n):
+    """Sampler fused into the pipeline: samples [first, first+n) of the
+    counter-based stream, never materialised as AoS."""
+    m = Model.mixed(13)
+    full, _ = ref.draw_batch(m, first + n)
+    want, _, _ = ref.run(full[first:], World(), "parallel")
+    rep, clamps = executor.run_model(to_model(m), n, first=first, chunk=4096)
+    assert_parity(ref, want, rep.results)
+    _, ref_clamps_prefix = ref.draw_batch(m, first) if first else (None, 0)
+    assert clamps == ref.draw_batch(m, first + n)[1] - ref_clamps_prefix
+    assert rep.chunks == (n + 4095) // 4096
+
+
+def test_run_model_device_outputs(ref, executor):
+    import torch
+    n = 30000
+    m = Model(seed=4)
+    samples, _ = ref.draw_batch(m, n)
+    want, _, _ = ref.run(samples, World(), "parallel")
+    d = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = torch.empty(n, dtype=torch.int32, device="cuda")
+    hz = torch.empty(n, dtype=torch.uint8, device="cuda")
+    rep, _ = executor.run_model(to_model(m), n, device_out=(d, st, hz), chunk=7000)
+    assert rep.results is None and rep.d2h_bytes == 0
+    assert np.array_equal(d.cpu().numpy().view(np.uint64), want["stop_distance"].view(np.uint64))
+    assert np.array_equal(st.cpu().numpy().astype(np.int64), want["steps"])
+    assert np.array_equal(hz.cpu().numpy(), want["hit_horizon"])
+
+
+def test_graph_mode_decisions(ref, executor):
+    g = executor.graph(25000)
+    try:
+        for seed in (1, 2):
+            s, _ = ref.draw_batch(Model(seed=seed), 25000)
+            want, _, _ = ref.run(s, World(), "parallel")
+            rep = g.run(s)
+            assert_parity(ref, want, rep.results)
+            assert rep.total_steps == int(want["steps"].sum())
+        # sampling inside the decision (feasibility convention)
+        rep = g.run_model(to_model(Model(seed=5)))
+        s, _ = ref.draw_batch(Model(seed=5), 25000)
+        want, _, _ = ref.run(s, World(), "parallel")
+        assert_parity(ref, want, rep.results)
+        # an unrelated larger call must not disturb the graph's buffers
+        big, _ = ref.draw_batch(Model.mixed(2), 50000)
+        executor.run(big, bmc.SimWorld(actuator_tau=0.3))
+        assert_parity(ref, want, g.run(s).results)
+    finally:
+        g.close()
+
+
+def test_feasibility_search_logic():
+    # analysis.cpp:258-318 with the reference test's synthetic linear machine
+    # t(n) = 0.01 + 1e-6 n (test_analysis.cpp:235-266)
+    n, capped = bmc.engine.max_feasible_n(lambda k: 0.01 + 1e-6 * k, 0.53, 1000, 1 << 22)
+    assert not capped and abs(n - 520000) <= 520000 // 64 + 1
+    n, capped = bmc.engine.max_feasible_n(lambda k: 0.0, 0.53, 1000, 4096)
+    assert capped and n == 4096
+    assert bmc.engine.max_feasible_n(lambda k: 1.0, 0.53, 1000, 4096) == (0, False)
