@@ -48,6 +48,7 @@ struct CudaExecOptions {
     int schedule = 0;             ///< 0 default, 1 index order, 2 binned (timing only)
     int block_threads = 0;        ///< 0 default (timing only)
     int table_mode = 0;           ///< 0 auto (timing only)
+    int ilp = 0;                  ///< samples per thread, 0 default (timing only)
 };
 
 static_assert(sizeof(ScenarioSample) == sizeof(bmc_sample), "ScenarioSample layout");
@@ -120,6 +121,7 @@ inline ExecutionReport run_cuda(const SampleBatch& batch, const SimConfig& confi
     opts.table_mode = options.table_mode;
     opts.host_threads = options.host_threads;
     opts.chunk_samples = options.chunk_samples;
+    opts.ilp = options.ilp;
 
     std::vector<bmc_ctx*> ctxs;
     for (int d : devices) ctxs.push_back(cuda_detail::context(d));

@@ -103,6 +103,8 @@ typedef struct {
     int32_t table_mode;     /* 0 = auto, 1 = shared-mem a-table, 2 = global a-table, 3 = no table */
     int32_t host_threads;   /* 0 = all hardware threads (host staging / unpack) */
     uint64_t chunk_samples; /* 0 = default pipeline chunk for bmc_cuda_run */
+    int32_t ilp;            /* samples per thread: 0 = default, 1, or 2 (table modes) */
+    int32_t reserved_;
 } bmc_run_opts;
 
 /* Timing breakdown of one bmc_cuda_run call (seconds). */

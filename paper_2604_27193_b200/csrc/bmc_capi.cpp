@@ -21,6 +21,8 @@ constexpr size_t kTableCap = size_t{1} << 20;          // 32 MB of stage values
 constexpr uint64_t kDefaultChunk = uint64_t{1} << 22;  // 4M samples per pipeline slot
 constexpr int kMaxCoarseSteps = 2048;
 constexpr int kBucketsTarget = 2000;  // step buckets; x2 clamp classes <= 4096 keys
+constexpr int kDefaultIlp = 1;
+constexpr int kDefaultIlp2Block = 640;
 
 bool same_key(const WorldDerived& a, const WorldDerived& b) {
     return std::memcmp(&a, &b, sizeof a) == 0;
@@ -102,14 +104,22 @@ int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uin
     int sched = opts.schedule;
     if (sched == kScheduleDefault) sched = kScheduleBinned;
     if (ctx->coarse_len == 0 || mode == kTableNone) sched = kScheduleIndex;
+    int ilp = opts.ilp == 0 ? kDefaultIlp : opts.ilp;
+    if (ilp != 1 && ilp != 2) return fail(ctx, BMC_E_CONFIG, "execution.ilp: must be 1 or 2");
+    if (mode == kTableNone) ilp = 1;
     int bt = opts.block_threads;
-    if (bt == 0) bt = mode == kTableGlobal ? 256 : 1024;
-    if (bt != 256 && bt != 512 && bt != 768 && bt != 1024) {
-        return fail(ctx, BMC_E_CONFIG, "execution.block_threads: must be 256, 512, 768 or 1024");
+    if (bt == 0) bt = ilp == 2 ? kDefaultIlp2Block : (mode == kTableGlobal ? 256 : 1024);
+    const bool ok_bt = ilp == 2 ? (bt == 512 || bt == 640 || bt == 768)
+                                : (bt == 256 || bt == 512 || bt == 768 || bt == 1024);
+    if (!ok_bt) {
+        return fail(ctx, BMC_E_CONFIG,
+                    ilp == 2 ? "execution.block_threads: must be 512, 640 or 768 with ilp 2"
+                             : "execution.block_threads: must be 256, 512, 768 or 1024");
     }
     p.mode = mode;
     p.sched = sched;
     p.bt = bt;
+    p.ilp = ilp;
     p.table = ctx->d_table.as<StageA>();
     p.table_len = ctx->t_len;
     p.table_min = ctx->t_min;
@@ -196,7 +206,7 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
     ra.counters = reinterpret_cast<unsigned long long*>(sc.counter.as<char>() + 8);
     if (ev) BMC_CK(ctx, cudaEventRecord(ev->r0, s));
     if (n > 0) {
-        BMC_CK(ctx, launch_rollout(ra, plan.mode, plan.bt, s));
+        BMC_CK(ctx, launch_rollout(ra, plan.mode, plan.bt, plan.ilp, s));
         ++nl;
     }
     if (ev) BMC_CK(ctx, cudaEventRecord(ev->r1, s));

@@ -94,6 +94,7 @@ struct Plan {
     int mode = kTableNone;
     int sched = kScheduleIndex;
     int bt = 1024;
+    int ilp = 1;
     const StageA* table = nullptr;
     int table_len = 0;
     double table_min = 0.0;

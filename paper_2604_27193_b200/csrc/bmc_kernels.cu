@@ -133,44 +133,171 @@ struct LaneOut {
 //   V2 [cmin_w, cmax_w)  brake = n < c_s ? table : floor (crossover band)
 //   V3 [.., max_steps)   brake = per-lane constants      (all lanes clamped, or
 //                        past the actuator fixed point)
+struct Chain {
+    double x, v, D, G, F;
+    int c0, c1, c2, c3;
+};
+
 template <int MODE>
-__device__ __forceinline__ LaneOut run_table(const RolloutArgs& A, const StageA* tab, int len,
-                                             uint64_t j, unsigned mask) {
-    const double D = A.drag[j];
-    const double G = A.grade[j];
-    const double F = A.brake_floor[j];
-    double v = A.v0[j];
-    double x = 0.0;
-    const int32_t M = A.max_steps;
-    const int c0 = crossover<MODE>(tab, len, 0, F), c1 = crossover<MODE>(tab, len, 1, F);
-    const int c2 = crossover<MODE>(tab, len, 2, F), c3 = crossover<MODE>(tab, len, 3, F);
-    const int cmin = min(min(c0, c1), min(c2, c3));
-    const int cmax = max(max(c0, c1), max(c2, c3));
-    const int head = min(len - 1, M);
-    const int p1 = min(static_cast<int>(__reduce_min_sync(mask, static_cast<unsigned>(cmin))), head);
-    const int p2 = min(static_cast<int>(__reduce_max_sync(mask, static_cast<unsigned>(cmax))), head);
-    int32_t n = 0;
-    for (; n < p1; ++n) {
-        const StageA s = load_stage<MODE>(tab, n);
-        rk4_xv(x, v, s.a0, s.a1, s.a2, s.a3, D, G, A.dt, A.half, A.sixth);
-        if (not_positive(v)) return LaneOut{x, n + 1, true};
+__device__ __forceinline__ void load_chain(const RolloutArgs& A, const StageA* tab, int len,
+                                           uint64_t j, bool ok, Chain& c) {
+    if (ok) {
+        c.D = A.drag[j];
+        c.G = A.grade[j];
+        c.F = A.brake_floor[j];
+        c.v = A.v0[j];
+        c.c0 = crossover<MODE>(tab, len, 0, c.F);
+        c.c1 = crossover<MODE>(tab, len, 1, c.F);
+        c.c2 = crossover<MODE>(tab, len, 2, c.F);
+        c.c3 = crossover<MODE>(tab, len, 3, c.F);
+    } else {
+        // inert filler: stops after one step, never clamps, never written
+        c.D = 0.0;
+        c.G = 0.0;
+        c.F = 0.0;
+        c.v = -1.0;
+        c.c0 = c.c1 = c.c2 = c.c3 = INT_MAX;
     }
-    for (; n < p2; ++n) {
-        const StageA s = load_stage<MODE>(tab, n);
-        rk4_xv(x, v, n < c0 ? s.a0 : F, n < c1 ? s.a1 : F, n < c2 ? s.a2 : F,
-               n < c3 ? s.a3 : F, D, G, A.dt, A.half, A.sixth);
-        if (not_positive(v)) return LaneOut{x, n + 1, true};
+    c.x = 0.0;
+}
+
+__device__ __forceinline__ int chain_cmin(const Chain& c) {
+    return min(min(c.c0, c.c1), min(c.c2, c.c3));
+}
+__device__ __forceinline__ int chain_cmax(const Chain& c) {
+    return max(max(c.c0, c.c1), max(c.c2, c.c3));
+}
+
+// The step loop of one chain from step n (its state after n steps) with the
+// warp-uniform phase bounds p1 <= p2 <= head.
+template <int MODE>
+__device__ __forceinline__ LaneOut steps_from(const RolloutArgs& A, const StageA* tab, int len,
+                                              Chain& c, int32_t n, int p1, int p2) {
+    const int32_t M = A.max_steps;
+    if (n < p2) {
+        // the next table row is fetched one step ahead (n + 1 <= head <= len - 1)
+        StageA nx = load_stage<MODE>(tab, n);
+        for (; n < p1; ++n) {
+            const StageA s = nx;
+            nx = load_stage<MODE>(tab, n + 1);
+            rk4_xv(c.x, c.v, s.a0, s.a1, s.a2, s.a3, c.D, c.G, A.dt, A.half, A.sixth);
+            if (not_positive(c.v)) return LaneOut{c.x, n + 1, true};
+        }
+        for (; n < p2; ++n) {
+            const StageA s = nx;
+            nx = load_stage<MODE>(tab, n + 1);
+            rk4_xv(c.x, c.v, n < c.c0 ? s.a0 : c.F, n < c.c1 ? s.a1 : c.F,
+                   n < c.c2 ? s.a2 : c.F, n < c.c3 ? s.a3 : c.F, c.D, c.G, A.dt, A.half,
+                   A.sixth);
+            if (not_positive(c.v)) return LaneOut{c.x, n + 1, true};
+        }
     }
     if (n < M) {
         const StageA s = load_stage<MODE>(tab, len - 1);
-        const double b0 = c0 <= n ? F : s.a0, b1 = c1 <= n ? F : s.a1;
-        const double b2 = c2 <= n ? F : s.a2, b3 = c3 <= n ? F : s.a3;
+        const double b0 = c.c0 <= n ? c.F : s.a0, b1 = c.c1 <= n ? c.F : s.a1;
+        const double b2 = c.c2 <= n ? c.F : s.a2, b3 = c.c3 <= n ? c.F : s.a3;
         for (; n < M; ++n) {
-            rk4_xv(x, v, b0, b1, b2, b3, D, G, A.dt, A.half, A.sixth);
-            if (not_positive(v)) return LaneOut{x, n + 1, true};
+            rk4_xv(c.x, c.v, b0, b1, b2, b3, c.D, c.G, A.dt, A.half, A.sixth);
+            if (not_positive(c.v)) return LaneOut{c.x, n + 1, true};
         }
     }
-    return LaneOut{x, M, false};
+    return LaneOut{c.x, M, false};
+}
+
+template <int MODE>
+__device__ __forceinline__ LaneOut run_table(const RolloutArgs& A, const StageA* tab, int len,
+                                             uint64_t j, unsigned mask) {
+    Chain c;
+    load_chain<MODE>(A, tab, len, j, true, c);
+    const int head = min(len - 1, A.max_steps);
+    const int p1 = min(__reduce_min_sync(mask, chain_cmin(c)), head);
+    const int p2 = min(__reduce_max_sync(mask, chain_cmax(c)), head);
+    return steps_from<MODE>(A, tab, len, c, 0, p1, p2);
+}
+
+// Two independent samples per thread (ILP = 2): the lanes of a warp own a
+// sorted 64-sample group (i and i + 32), so both chains of a thread stop
+// within a few steps of each other.  Both chains step together until the
+// first one stops (one combined termination test per step, no per-chain
+// latching in the hot loop); the survivor then finishes on the single-chain
+// loop from that step.  Shared per-thread state (table row, loop control)
+// is amortised over two dependency chains.
+template <int MODE>
+__device__ __forceinline__ void run_table2(const RolloutArgs& A, const StageA* tab, int len,
+                                           uint64_t j0, uint64_t j1, bool ok0, bool ok1,
+                                           LaneOut& r0, LaneOut& r1) {
+    Chain a, b;
+    load_chain<MODE>(A, tab, len, j0, ok0, a);
+    load_chain<MODE>(A, tab, len, j1, ok1, b);
+    const int32_t M = A.max_steps;
+    const int head = min(len - 1, M);
+    const int lmin = min(ok0 ? chain_cmin(a) : INT_MAX, ok1 ? chain_cmin(b) : INT_MAX);
+    const int lmax = max(ok0 ? chain_cmax(a) : INT_MIN, ok1 ? chain_cmax(b) : INT_MIN);
+    const int p1 = min(__reduce_min_sync(0xffffffffu, lmin), head);
+    const int p2 = max(min(__reduce_max_sync(0xffffffffu, lmax), head), p1);
+    int32_t n = 0;
+    bool hit = false;
+    if (n < p2) {
+        StageA nx = load_stage<MODE>(tab, 0);
+        for (; n < p1; ++n) {
+            const StageA s = nx;
+            nx = load_stage<MODE>(tab, n + 1);
+            rk4_xv(a.x, a.v, s.a0, s.a1, s.a2, s.a3, a.D, a.G, A.dt, A.half, A.sixth);
+            rk4_xv(b.x, b.v, s.a0, s.a1, s.a2, s.a3, b.D, b.G, A.dt, A.half, A.sixth);
+            if (not_positive(a.v) | not_positive(b.v)) {
+                hit = true;
+                break;
+            }
+        }
+        if (!hit) {
+            for (; n < p2; ++n) {
+                const StageA s = nx;
+                nx = load_stage<MODE>(tab, n + 1);
+                rk4_xv(a.x, a.v, n < a.c0 ? s.a0 : a.F, n < a.c1 ? s.a1 : a.F,
+                       n < a.c2 ? s.a2 : a.F, n < a.c3 ? s.a3 : a.F, a.D, a.G, A.dt, A.half,
+                       A.sixth);
+                rk4_xv(b.x, b.v, n < b.c0 ? s.a0 : b.F, n < b.c1 ? s.a1 : b.F,
+                       n < b.c2 ? s.a2 : b.F, n < b.c3 ? s.a3 : b.F, b.D, b.G, A.dt, A.half,
+                       A.sixth);
+                if (not_positive(a.v) | not_positive(b.v)) {
+                    hit = true;
+                    break;
+                }
+            }
+        }
+    }
+    if (!hit && n < M) {
+        const StageA s = load_stage<MODE>(tab, len - 1);
+        const double a0 = a.c0 <= n ? a.F : s.a0, a1 = a.c1 <= n ? a.F : s.a1;
+        const double a2 = a.c2 <= n ? a.F : s.a2, a3 = a.c3 <= n ? a.F : s.a3;
+        const double b0 = b.c0 <= n ? b.F : s.a0, b1 = b.c1 <= n ? b.F : s.a1;
+        const double b2 = b.c2 <= n ? b.F : s.a2, b3 = b.c3 <= n ? b.F : s.a3;
+        for (; n < M; ++n) {
+            rk4_xv(a.x, a.v, a0, a1, a2, a3, a.D, a.G, A.dt, A.half, A.sixth);
+            rk4_xv(b.x, b.v, b0, b1, b2, b3, b.D, b.G, A.dt, A.half, A.sixth);
+            if (not_positive(a.v) | not_positive(b.v)) {
+                hit = true;
+                break;
+            }
+        }
+    }
+    if (!hit) {  // both reached the horizon
+        r0 = LaneOut{a.x, M, false};
+        r1 = LaneOut{b.x, M, false};
+        return;
+    }
+    const bool sa = not_positive(a.v), sb = not_positive(b.v);
+    if (sa) r0 = LaneOut{a.x, n + 1, true};
+    if (sb) r1 = LaneOut{b.x, n + 1, true};
+    if (sa && sb) return;
+    // finish the survivor from step n + 1 on the single-chain loop
+    Chain& c = sa ? b : a;
+    const LaneOut r = steps_from<MODE>(A, tab, len, c, n + 1, p1, p2);
+    if (sa) {
+        r1 = r;
+    } else {
+        r0 = r;
+    }
 }
 
 // Generic path (no usable table): the actuator lane is integrated inline
@@ -194,7 +321,7 @@ __device__ __forceinline__ LaneOut run_inline(const RolloutArgs& A, uint64_t j) 
     return LaneOut{x, M, false};
 }
 
-template <int MODE, int BT>
+template <int MODE, int BT, int ILP>
 __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const StageA* tab = A.table;
@@ -212,8 +339,34 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
         unsigned g = 0;
         if (lane == 0) g = atomicAdd(A.work_counter, 1u);
         g = __shfl_sync(0xffffffffu, g, 0);
-        const uint64_t base = static_cast<uint64_t>(g) * 32u;
+        const uint64_t base = static_cast<uint64_t>(g) * (32u * ILP);
         if (base >= A.n) break;
+        if (ILP == 2) {
+            const uint64_t i0 = base + lane, i1 = i0 + 32u;
+            const bool ok0 = i0 < A.n, ok1 = i1 < A.n;
+            const uint64_t j0 = ok0 ? (A.perm ? static_cast<uint64_t>(A.perm[i0]) : i0) : 0;
+            const uint64_t j1 = ok1 ? (A.perm ? static_cast<uint64_t>(A.perm[i1]) : i1) : 0;
+            LaneOut r0, r1;
+            run_table2<MODE>(A, tab, len, j0, j1, ok0, ok1, r0, r1);
+            if (ok0) {
+                if (A.stop_distance) A.stop_distance[j0] = r0.x;
+                if (A.steps) A.steps[j0] = r0.steps;
+                if (A.hit_horizon) A.hit_horizon[j0] = r0.stopped ? 0 : 1;
+                my_steps += static_cast<unsigned>(max(r0.steps, 0));
+            }
+            if (ok1) {
+                if (A.stop_distance) A.stop_distance[j1] = r1.x;
+                if (A.steps) A.steps[j1] = r1.steps;
+                if (A.hit_horizon) A.hit_horizon[j1] = r1.stopped ? 0 : 1;
+                my_steps += static_cast<unsigned>(max(r1.steps, 0));
+            }
+            const int lmax = max(ok0 ? r0.steps : 0, ok1 ? r1.steps : 0);
+            const unsigned gmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(max(lmax, 0)));
+            const unsigned chains = __popc(__ballot_sync(0xffffffffu, ok0)) +
+                                    __popc(__ballot_sync(0xffffffffu, ok1));
+            if (lane == 0) my_slots += static_cast<unsigned long long>(gmax) * chains;
+            continue;
+        }
         const uint64_t i = base + lane;
         const unsigned mask = __ballot_sync(0xffffffffu, i < A.n);
         if (i < A.n) {
@@ -359,27 +512,27 @@ __global__ void __launch_bounds__(512) fp64_probe_kernel(double* out, int iters,
     if (s == 12345.678) out[0] = s;  // never true; keeps the chains alive
 }
 
-template <int MODE, int BT>
+template <int MODE, int BT, int ILP>
 cudaError_t launch_rollout_t(const RolloutArgs& a, cudaStream_t s) {
     size_t smem = 0;
     if (MODE == kTableShared) {
         smem = static_cast<size_t>(a.table_len) * sizeof(StageA);
-        const cudaError_t e = cudaFuncSetAttribute(rollout_kernel<MODE, BT>,
+        const cudaError_t e = cudaFuncSetAttribute(rollout_kernel<MODE, BT, ILP>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
     int dev = 0, per_sm = 0;
     cudaGetDevice(&dev);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rollout_kernel<MODE, BT>,
-                                                                  BT, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, rollout_kernel<MODE, BT, ILP>, BT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     // Persistent grid.  Small batches (the real-time case) spread their
-    // 32-sample groups over every SM with narrower CTAs instead of packing
+    // sample groups over every SM with narrower CTAs instead of packing
     // them into a few full ones: fewer warps per SM = shorter per-step
     // latency of each dependent RK4 chain.
-    const uint64_t groups = (a.n + 31) / 32;
+    const uint64_t groups = (a.n + 32 * ILP - 1) / (32 * ILP);
     const uint64_t sms = static_cast<uint64_t>(sm_count_cached(dev));
     const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
     uint64_t warps_per_block = BT / 32;
@@ -388,17 +541,25 @@ cudaError_t launch_rollout_t(const RolloutArgs& a, cudaStream_t s) {
     }
     const uint64_t need = (groups + warps_per_block - 1) / warps_per_block;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(need, resident)));
-    rollout_kernel<MODE, BT><<<grid, static_cast<int>(warps_per_block * 32), smem, s>>>(a);
+    rollout_kernel<MODE, BT, ILP><<<grid, static_cast<int>(warps_per_block * 32), smem, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int MODE>
-cudaError_t launch_rollout_m(const RolloutArgs& a, int block_threads, cudaStream_t s) {
+cudaError_t launch_rollout_m(const RolloutArgs& a, int block_threads, int ilp, cudaStream_t s) {
+    if (ilp == 2 && MODE != kTableNone) {
+        switch (block_threads) {
+            case 512: return launch_rollout_t<MODE, 512, 2>(a, s);
+            case 640: return launch_rollout_t<MODE, 640, 2>(a, s);
+            case 768: return launch_rollout_t<MODE, 768, 2>(a, s);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (block_threads) {
-        case 256: return launch_rollout_t<MODE, 256>(a, s);
-        case 512: return launch_rollout_t<MODE, 512>(a, s);
-        case 768: return launch_rollout_t<MODE, 768>(a, s);
-        case 1024: return launch_rollout_t<MODE, 1024>(a, s);
+        case 256: return launch_rollout_t<MODE, 256, 1>(a, s);
+        case 512: return launch_rollout_t<MODE, 512, 1>(a, s);
+        case 768: return launch_rollout_t<MODE, 768, 1>(a, s);
+        case 1024: return launch_rollout_t<MODE, 1024, 1>(a, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -418,11 +579,12 @@ int sm_count(int device) {
     return v;
 }
 
-cudaError_t launch_rollout(const RolloutArgs& a, int table_mode, int block_threads, cudaStream_t s) {
+cudaError_t launch_rollout(const RolloutArgs& a, int table_mode, int block_threads, int ilp,
+                           cudaStream_t s) {
     switch (table_mode) {
-        case kTableShared: return launch_rollout_m<kTableShared>(a, block_threads, s);
-        case kTableGlobal: return launch_rollout_m<kTableGlobal>(a, block_threads, s);
-        case kTableNone: return launch_rollout_m<kTableNone>(a, block_threads, s);
+        case kTableShared: return launch_rollout_m<kTableShared>(a, block_threads, ilp, s);
+        case kTableGlobal: return launch_rollout_m<kTableGlobal>(a, block_threads, ilp, s);
+        case kTableNone: return launch_rollout_m<kTableNone>(a, block_threads, 1, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -150,8 +150,9 @@ class CudaExecutor:
         N.check(rc, self.ctx)
 
     @staticmethod
-    def _opts(schedule="default", block_threads=0, table="auto", host_threads=0, chunk=0):
-        return N.RunOpts(SCHEDULE[schedule], block_threads, TABLE[table], host_threads, chunk)
+    def _opts(schedule="default", block_threads=0, table="auto", host_threads=0, chunk=0, ilp=0):
+        return N.RunOpts(SCHEDULE[schedule], block_threads, TABLE[table], host_threads, chunk,
+                         ilp, 0)
 
     # -------------------------------------------------------------- executor
     def run(self, samples: np.ndarray, world: SimWorld = SimWorld(), out: np.ndarray = None,

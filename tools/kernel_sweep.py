@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--model", default="default")
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
     n = int(a.samples)
     model = bmc.UncertaintyModel.mixed(3) if a.model == "mixed" else bmc.UncertaintyModel(seed=3)
@@ -43,16 +44,20 @@ def main():
             ex.sync()
         print("profile run done", ex.last_kernel_ms())
         return
-    configs = list(itertools.product(["binned", "index"], ["shared", "global", "none"],
-                                     [256, 512, 768, 1024]))
-    for sched, table, bt in configs:
+    configs = [(s, t, b, 1) for s, t, b in itertools.product(
+        ["binned", "index"], ["shared", "global", "none"], [256, 512, 768, 1024])]
+    configs += [(s, t, b, 2) for s, t, b in itertools.product(
+        ["binned"], ["shared", "global"], [512, 640, 768])]
+    if a.quick:
+        configs = [c for c in configs if c[0] == "binned" and c[2] >= 512 and c[1] != "none"]
+    for sched, table, bt, ilp in configs:
         if table == "none" and sched == "binned":
             continue
         best = None
         for _ in range(a.reps):
             tot.zero_()
             ex.rollout_device(dev, (d, st, hz), total_steps=tot, schedule=sched, table=table,
-                              block_threads=bt)
+                              block_threads=bt, ilp=ilp)
             ex.sync()
             r, p = ex.last_kernel_ms()
             if best is None or r + p < best[0] + best[1]:
@@ -60,7 +65,7 @@ def main():
         steps = int(tot.item())
         r, p = best
         _, _, eff = ex.lane_efficiency()
-        print(f"{a.model:7s} n={n} sched={sched:6s} table={table:6s} bt={bt:4d}  "
+        print(f"{a.model:7s} n={n} sched={sched:6s} table={table:6s} bt={bt:4d} ilp={ilp} "
               f"rollout {r:9.3f} ms  predict {p:7.3f} ms  steps/s {steps/(r*1e-3):.4e}  "
               f"exec-op/s {32*steps/(r*1e-3)/1e12:.3f} T ({32*steps/(r*1e-3)/peak:.3f} of probe)"
               f"  algo {57*steps/(r*1e-3)/peak:.3f}  lane-eff {eff:.4f}", flush=True)
