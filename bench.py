@@ -261,22 +261,47 @@ def b200_arm(args, rank, world, local_rank, dist):
     launches = [0]
     kernel_ms = []
 
+    from paper_2604_27193_b200 import distributed as D
+    coll = D.Collective(dist if world > 1 else None, f"cuda:{local_rank}")
+
+    class CountingShard(D.DeviceShard):
+        """DeviceShard that tallies the kernels each statistic launches."""
+
+        def _n(self, r):
+            launches[1] += self.ex.last_launches()
+            return r
+
+        def partials(self):
+            return self._n(super().partials())
+
+        def moments(self, mean):
+            return self._n(super().moments(mean))
+
+        def histogram(self, origin, bw, bins):
+            return self._n(super().histogram(origin, bw, bins))
+
+        def exceedance(self, headways):
+            return self._n(super().exceedance(headways))
+
+        def select_pass(self, exclude, shift, prefixes):
+            return self._n(super().select_pass(exclude, shift, prefixes))
+
+    shard = CountingShard(ex, d, hz)
+    launches.append(0)
+
     def step(record=False):
         total_steps.zero_()
         ex.rollout_device(dev_terms, (d, st, hz), sw, total_steps=total_steps)
         nl = ex.last_launches()
-        counts = ex.exceedance_counts(d, hz, headways)
-        nl += ex.last_launches()
         if record:
             kernel_ms.append(ex.last_kernel_ms()[0])
-        summ = ex.summarize(d, hz, 2.0)
-        nl += ex.last_launches()
-        vec = torch.tensor(list(counts) + [summ["horizon_count"]], dtype=torch.int64,
-                           device=f"cuda:{local_rank}")
-        if world > 1:
-            dist.all_reduce(vec)
-        launches[0] += nl if record else 0
-        return vec, summ
+        launches[1] = 0
+        # statistics merged over all ranks (one allreduce per quantity)
+        counts = D.exceedance_counts(shard, coll, headways)
+        summ = D.summarize(shard, coll, 2.0)
+        if record:
+            launches[0] += nl + launches[1]
+        return counts, summ
 
     for _ in range(args.warmup):
         step()
@@ -306,6 +331,14 @@ def b200_arm(args, rank, world, local_rank, dist):
     value = n_total / (ms_per_step * 1e-3)
 
     roll_ms = sum(kernel_ms) / len(kernel_ms)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "rollout_traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        traffic = {"bytes_per_launch": tj["bytes_per_sample"] * n,
+                   "bytes_per_sample": tj["bytes_per_sample"],
+                   "algorithmic_bytes_per_sample": tj["algorithmic_bytes_per_sample"],
+                   "source": tj["source"] + ", scaled to this launch's sample count"}
     steps_per_launch = steps_sum / args.steps
     achieved = ALGO_FLOPS_PER_STEP * steps_per_launch / (roll_ms * 1e-3)
     executed = EXEC_FLOPS_PER_STEP * steps_per_launch / (roll_ms * 1e-3)
@@ -362,7 +395,7 @@ def b200_arm(args, rank, world, local_rank, dist):
                              % (32 * n / 1e9),
                        "sampling_s": sample_s, "clamp_count": clamps},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
-                         "unit": "TFLOP/s", "frac": achieved / peak_ops, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / peak_ops, "traffic": traffic,
                          "kernel": "rollout_kernel", "kernel_ms": roll_ms,
                          "rk4_steps_per_launch": steps_per_launch,
                          "algorithmic_flops_per_step": ALGO_FLOPS_PER_STEP,

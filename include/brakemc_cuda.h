@@ -184,7 +184,7 @@ int bmc_cuda_rollout_device(bmc_ctx* ctx, const bmc_terms* terms, size_t n,
                             void* stream);
 
 /* Last rollout kernel's device time in ms, via CUDA events recorded around
- * it on its own stream (valid after the stream is synchronised). */
+ * it on its own stream (waits for the closing event). */
 int bmc_cuda_last_kernel_ms(bmc_ctx* ctx, float* rollout_ms, float* predict_ms);
 /* Executed RK4 steps and lane slots (sum over 32-sample groups of
  * active lanes x longest lane) of the last rollout launch on the context's
@@ -220,6 +220,32 @@ int bmc_cuda_exceedance(bmc_ctx* ctx, const double* stop_distance, const uint8_t
 int bmc_cuda_order_stats(bmc_ctx* ctx, const double* stop_distance, const uint8_t* hit_horizon,
                          size_t n, int exclude_horizon, const uint64_t* ranks, size_t m,
                          double* out, uint64_t* count_out);
+
+/* Mergeable building blocks for sharded (multi-GPU) statistics: counts add,
+ * extrema take min/max, double-double sums merge exactly, so one allreduce
+ * per quantity combines shards.  All inputs are device
+ * pointers; outputs are host. */
+typedef struct {
+    uint64_t count, horizon_count;
+    double min, max;          /* +inf / -inf for an empty shard */
+    double sum_hi, sum_lo;    /* double-double sum of stop_distance */
+    int32_t any_nan;
+    int32_t pad_;
+} bmc_partials;
+int bmc_cuda_partials(bmc_ctx* ctx, const double* stop_distance, const uint8_t* hit_horizon,
+                      size_t n, bmc_partials* out);
+/* m2m3[4] = (sum dev^2 hi, lo, sum dev^3 hi, lo) with dev = d - mean */
+int bmc_cuda_moments(bmc_ctx* ctx, const double* stop_distance, size_t n, double mean,
+                     double* m2m3);
+/* counts[bins]: idx = (size_t)((d - origin) / bin_width) clamped to bins-1
+ * (analysis.cpp:61-75 with a caller-chosen origin and bin count) */
+int bmc_cuda_histogram(bmc_ctx* ctx, const double* stop_distance, size_t n, double origin,
+                       double bin_width, uint64_t bins, uint64_t* counts);
+/* One 8-bit radix-select pass: hist[t*256 + digit] counts the candidates whose
+ * order key matches prefixes[t] above bit shift+8 (shift = 56, 48, ..., 0). */
+int bmc_cuda_select_pass(bmc_ctx* ctx, const double* stop_distance, const uint8_t* hit_horizon,
+                         size_t n, int exclude_horizon, int shift, const uint64_t* prefixes,
+                         size_t m, uint64_t* hist);
 
 /* ------------------------------------------------------- measurement */
 /* FP64 DADD/DMUL issue-rate probe (the rollout's roofline denominator;

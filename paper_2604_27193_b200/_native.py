@@ -91,6 +91,12 @@ class Summary(C.Structure):
                 ("pad_", C.c_int32)]
 
 
+class Partials(C.Structure):
+    _fields_ = [("count", C.c_uint64), ("horizon_count", C.c_uint64), ("min", C.c_double),
+                ("max", C.c_double), ("sum_hi", C.c_double), ("sum_lo", C.c_double),
+                ("any_nan", C.c_int32), ("pad_", C.c_int32)]
+
+
 assert C.sizeof(Sample) == 40 and C.sizeof(Result) == 32 and C.sizeof(Model) == 88
 
 # (name, restype, argtypes) for every entry point declared in brakemc_cuda.h
@@ -131,6 +137,12 @@ SIGNATURES = [
                                        C.POINTER(C.c_uint64)]),
     ("bmc_cuda_fp64_peak", C.c_int, [_P, C.c_int, C.POINTER(C.c_double),
                                      C.POINTER(C.c_double)]),
+    ("bmc_cuda_partials", C.c_int, [_P, _P, _P, C.c_size_t, C.POINTER(Partials)]),
+    ("bmc_cuda_moments", C.c_int, [_P, _P, C.c_size_t, C.c_double, _P]),
+    ("bmc_cuda_histogram", C.c_int, [_P, _P, C.c_size_t, C.c_double, C.c_double, C.c_uint64,
+                                     _P]),
+    ("bmc_cuda_select_pass", C.c_int, [_P, _P, _P, C.c_size_t, C.c_int, C.c_int, _P,
+                                       C.c_size_t, _P]),
 ]
 
 _lib = None

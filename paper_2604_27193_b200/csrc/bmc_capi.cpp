@@ -134,9 +134,12 @@ int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n) {
     // counter: [0] work counter (u32) | [8] executed steps | [16] lane slots
     BMC_CK(ctx, sc.counter.reserve(64));
     if (plan.sched == kScheduleBinned) {
-        BMC_CK(ctx, sc.keys.reserve(std::max<uint64_t>(n, 1) * sizeof(uint16_t)));
-        BMC_CK(ctx, sc.perm.reserve(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
+        const uint64_t m = std::max<uint64_t>(n, 1);
+        BMC_CK(ctx, sc.keys.reserve(m * sizeof(uint16_t)));
+        BMC_CK(ctx, sc.perm.reserve(m * sizeof(uint32_t)));  // inverse permutation
         BMC_CK(ctx, sc.hist.reserve(4096 * sizeof(unsigned int)));
+        BMC_CK(ctx, sc.packed_in.reserve(m * sizeof(PackedTerms)));
+        BMC_CK(ctx, sc.packed_out.reserve(m * sizeof(PackedOut)));
     }
     return BMC_OK;
 }
@@ -151,7 +154,7 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
     if (rc != BMC_OK) return rc;
     const WorldDerived& d = plan.d;
     uint32_t nl = 0;
-    const uint32_t* perm = nullptr;
+    bool packed = false;
     if (ev) ev->predicted = false;
     if (plan.sched == kScheduleBinned && n > 0) {
         const int buckets = bucket_count(d);
@@ -176,10 +179,12 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
         BMC_CK(ctx, launch_predict(pa, s));
         BMC_CK(ctx, launch_bin_scan(sc.hist.as<unsigned int>(), buckets, s));
         BMC_CK(ctx, launch_bin_scatter(sc.keys.as<uint16_t>(), n, sc.hist.as<unsigned int>(),
+                                       terms.initial_speed, terms.brake_floor, terms.drag_factor,
+                                       terms.grade_accel, sc.packed_in.as<PackedTerms>(),
                                        sc.perm.as<uint32_t>(), s));
         if (ev) BMC_CK(ctx, cudaEventRecord(ev->p1, s));
         nl += 3;
-        perm = sc.perm.as<uint32_t>();
+        packed = true;
         if (ev) ev->predicted = true;
     }
     BMC_CK(ctx, cudaMemsetAsync(sc.counter.p, 0, 24, s));
@@ -188,7 +193,9 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
     ra.brake_floor = terms.brake_floor;
     ra.drag = terms.drag_factor;
     ra.grade = terms.grade_accel;
-    ra.perm = perm;
+    ra.perm = nullptr;
+    ra.packed_in = packed ? sc.packed_in.as<PackedTerms>() : nullptr;
+    ra.packed_out = packed ? sc.packed_out.as<PackedOut>() : nullptr;
     ra.n = n;
     ra.dt = d.dt;
     ra.half = d.half;
@@ -210,6 +217,11 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
         ++nl;
     }
     if (ev) BMC_CK(ctx, cudaEventRecord(ev->r1, s));
+    if (packed && n > 0 && (out.stop_distance || out.steps || out.hit_horizon)) {
+        BMC_CK(ctx, launch_unpermute(sc.packed_out.as<PackedOut>(), sc.perm.as<uint32_t>(), n,
+                                     out.stop_distance, out.steps, out.hit_horizon, s));
+        ++nl;
+    }
     if (launches) *launches += nl;
     return BMC_OK;
 }
@@ -490,6 +502,7 @@ int bmc_cuda_last_kernel_ms(bmc_ctx* ctx, float* rollout_ms, float* predict_ms) 
     int rc = bmc::prepare(ctx);
     if (rc) return rc;
     float r = 0.0f, p = 0.0f;
+    BMC_CK(ctx, cudaEventSynchronize(ctx->kev.r1));
     BMC_CK(ctx, cudaEventElapsedTime(&r, ctx->kev.r0, ctx->kev.r1));
     if (ctx->kev.predicted) BMC_CK(ctx, cudaEventElapsedTime(&p, ctx->kev.p0, ctx->kev.p1));
     if (rollout_ms) *rollout_ms = r;

@@ -247,4 +247,123 @@ int bmc_cuda_exceedance(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t
     return BMC_OK;
 }
 
+// ----------------------------------------------------------------------
+// Mergeable building blocks: every output below is exactly additive (counts)
+// or exactly mergeable (min/max, double-double sums) across shards, so a
+// multi-GPU run combines them with one allreduce per quantity.
+
+int bmc_cuda_partials(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n,
+                      bmc_partials* out) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!d || !out) return fail(ctx, BMC_E_CONFIG, "partials: null argument");
+    bmc_partials p;
+    std::memset(&p, 0, sizeof p);
+    p.min = std::numeric_limits<double>::infinity();
+    p.max = -std::numeric_limits<double>::infinity();
+    ctx->last_launches = 0;
+    if (n > 0) {
+        cudaStream_t s = ctx->stream;
+        const int P = bmc::stats_partials(n);
+        BMC_CK(ctx, ctx->partials.reserve(static_cast<size_t>(P) * sizeof(bmc::BlockPartial)));
+        std::vector<bmc::BlockPartial> parts(P);
+        BMC_CK(ctx, bmc::launch_reduce(d, hz, n, ctx->partials.as<bmc::BlockPartial>(), s));
+        BMC_CK(ctx, cudaMemcpyAsync(parts.data(), ctx->partials.p, P * sizeof(bmc::BlockPartial),
+                                    cudaMemcpyDeviceToHost, s));
+        BMC_CK(ctx, cudaStreamSynchronize(s));
+        ctx->last_launches = 1;
+        bmc::DDh sum;
+        for (const auto& q : parts) {
+            p.min = std::fmin(p.min, q.min);
+            p.max = std::fmax(p.max, q.max);
+            sum = bmc::dd_merge_h(sum, q.sum_hi, q.sum_lo);
+            p.horizon_count += q.horizon;
+            p.count += q.count;
+            p.any_nan |= q.nan;
+        }
+        p.sum_hi = sum.hi;
+        p.sum_lo = sum.lo;
+    }
+    *out = p;
+    return BMC_OK;
+}
+
+int bmc_cuda_moments(bmc_ctx* ctx, const double* d, size_t n, double mean, double* m2m3) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!d || !m2m3) return fail(ctx, BMC_E_CONFIG, "moments: null argument");
+    ctx->last_launches = 0;
+    bmc::DDh m2, m3;
+    if (n > 0) {
+        cudaStream_t s = ctx->stream;
+        const int P = bmc::stats_partials(n);
+        BMC_CK(ctx, ctx->partials.reserve(static_cast<size_t>(P) * sizeof(bmc::MomentPartial)));
+        std::vector<bmc::MomentPartial> mom(P);
+        BMC_CK(ctx, bmc::launch_moments(d, n, mean, ctx->partials.as<bmc::MomentPartial>(), s));
+        BMC_CK(ctx, cudaMemcpyAsync(mom.data(), ctx->partials.p, P * sizeof(bmc::MomentPartial),
+                                    cudaMemcpyDeviceToHost, s));
+        BMC_CK(ctx, cudaStreamSynchronize(s));
+        ctx->last_launches = 1;
+        for (const auto& q : mom) {
+            m2 = bmc::dd_merge_h(m2, q.m2_hi, q.m2_lo);
+            m3 = bmc::dd_merge_h(m3, q.m3_hi, q.m3_lo);
+        }
+    }
+    m2m3[0] = m2.hi;
+    m2m3[1] = m2.lo;
+    m2m3[2] = m3.hi;
+    m2m3[3] = m3.lo;
+    return BMC_OK;
+}
+
+int bmc_cuda_histogram(bmc_ctx* ctx, const double* d, size_t n, double origin, double bin_width,
+                       uint64_t bins, uint64_t* counts) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!d || !counts) return fail(ctx, BMC_E_CONFIG, "histogram: null argument");
+    if (!(bin_width > 0.0)) return fail(ctx, BMC_E_CONFIG, "outputs.bin_width: must be > 0");
+    if (bins == 0 || bins > (uint64_t{1} << 28)) return fail(ctx, BMC_E_RANGE, "histogram: bins out of range");
+    ctx->last_launches = 0;
+    cudaStream_t s = ctx->stream;
+    BMC_CK(ctx, ctx->hist_buf.reserve(bins * sizeof(unsigned long long)));
+    BMC_CK(ctx, cudaMemsetAsync(ctx->hist_buf.p, 0, bins * sizeof(unsigned long long), s));
+    if (n > 0) {
+        BMC_CK(ctx, bmc::launch_hist(d, n, origin, bin_width, bins, ctx->hist_buf.as<unsigned long long>(), s));
+        ctx->last_launches = 1;
+    }
+    BMC_CK(ctx, cudaMemcpyAsync(counts, ctx->hist_buf.p, bins * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    BMC_CK(ctx, cudaStreamSynchronize(s));
+    return BMC_OK;
+}
+
+int bmc_cuda_select_pass(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n,
+                         int exclude_horizon, int shift, const uint64_t* prefixes, size_t m,
+                         uint64_t* hist) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!d || !prefixes || !hist) return fail(ctx, BMC_E_CONFIG, "select_pass: null argument");
+    if (m < 1 || m > static_cast<size_t>(bmc::kMaxSelectTargets)) {
+        return fail(ctx, BMC_E_RANGE, "select_pass: 1..16 targets per pass");
+    }
+    if (shift < 0 || shift > 56 || shift % 8 != 0) return fail(ctx, BMC_E_CONFIG, "select_pass: shift must be 0, 8, ..., 56");
+    ctx->last_launches = 0;
+    cudaStream_t s = ctx->stream;
+    BMC_CK(ctx, ctx->sel_pref.reserve(bmc::kMaxSelectTargets * sizeof(uint64_t)));
+    BMC_CK(ctx, ctx->sel_hist.reserve(bmc::kMaxSelectTargets * 256 * sizeof(unsigned long long)));
+    BMC_CK(ctx, cudaMemcpyAsync(ctx->sel_pref.p, prefixes, m * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    BMC_CK(ctx, cudaMemsetAsync(ctx->sel_hist.p, 0, m * 256 * sizeof(unsigned long long), s));
+    if (n > 0) {
+        BMC_CK(ctx, bmc::launch_select(d, hz, n, exclude_horizon, shift, ctx->sel_pref.as<uint64_t>(),
+                                       static_cast<int>(m), ctx->sel_hist.as<unsigned long long>(), s));
+        ctx->last_launches = 1;
+    }
+    BMC_CK(ctx, cudaMemcpyAsync(hist, ctx->sel_hist.p, m * 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    BMC_CK(ctx, cudaStreamSynchronize(s));
+    return BMC_OK;
+}
+
 }  // extern "C"

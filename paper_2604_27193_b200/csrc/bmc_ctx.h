@@ -77,12 +77,14 @@ struct KernelEvents {
 // Device buffers one rollout launch needs besides its inputs/outputs.
 // A CUDA graph owns its own Scratch so captured pointers stay valid.
 struct Scratch {
-    DevBuf keys, perm, hist, counter;
+    DevBuf keys, perm, hist, counter, packed_in, packed_out;
     void release() {
         keys.release();
         perm.release();
         hist.release();
         counter.release();
+        packed_in.release();
+        packed_out.release();
     }
 };
 

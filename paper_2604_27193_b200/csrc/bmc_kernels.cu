@@ -126,6 +126,22 @@ struct LaneOut {
     bool stopped;
 };
 
+// One result: a packed 16-byte record in sorted order (binned schedule), or
+// the compact SoA outputs at the sample's index.
+__device__ __forceinline__ void store_out(const RolloutArgs& A, uint64_t j, const LaneOut& r) {
+    if (A.packed_out) {
+        PackedOut o;
+        o.x = r.x;
+        o.steps = r.steps;
+        o.hit_horizon = r.stopped ? 0u : 1u;
+        A.packed_out[j] = o;
+        return;
+    }
+    if (A.stop_distance) A.stop_distance[j] = r.x;
+    if (A.steps) A.steps[j] = r.steps;
+    if (A.hit_horizon) A.hit_horizon[j] = r.stopped ? 0 : 1;
+}
+
 // simulate_rollout (integrator.cpp:13-29) for sample j, table modes.  The
 // step loop is split at warp-uniform bounds so that almost every step runs
 // a body with no clamp selects at all:
@@ -142,10 +158,19 @@ template <int MODE>
 __device__ __forceinline__ void load_chain(const RolloutArgs& A, const StageA* tab, int len,
                                            uint64_t j, bool ok, Chain& c) {
     if (ok) {
-        c.D = A.drag[j];
-        c.G = A.grade[j];
-        c.F = A.brake_floor[j];
-        c.v = A.v0[j];
+        if (A.packed_in) {
+            const double2* p = reinterpret_cast<const double2*>(A.packed_in + j);
+            const double2 lo = __ldg(p), hi = __ldg(p + 1);
+            c.v = lo.x;
+            c.F = lo.y;
+            c.D = hi.x;
+            c.G = hi.y;
+        } else {
+            c.D = A.drag[j];
+            c.G = A.grade[j];
+            c.F = A.brake_floor[j];
+            c.v = A.v0[j];
+        }
         c.c0 = crossover<MODE>(tab, len, 0, c.F);
         c.c1 = crossover<MODE>(tab, len, 1, c.F);
         c.c2 = crossover<MODE>(tab, len, 2, c.F);
@@ -349,15 +374,11 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
             LaneOut r0, r1;
             run_table2<MODE>(A, tab, len, j0, j1, ok0, ok1, r0, r1);
             if (ok0) {
-                if (A.stop_distance) A.stop_distance[j0] = r0.x;
-                if (A.steps) A.steps[j0] = r0.steps;
-                if (A.hit_horizon) A.hit_horizon[j0] = r0.stopped ? 0 : 1;
+                store_out(A, j0, r0);
                 my_steps += static_cast<unsigned>(max(r0.steps, 0));
             }
             if (ok1) {
-                if (A.stop_distance) A.stop_distance[j1] = r1.x;
-                if (A.steps) A.steps[j1] = r1.steps;
-                if (A.hit_horizon) A.hit_horizon[j1] = r1.stopped ? 0 : 1;
+                store_out(A, j1, r1);
                 my_steps += static_cast<unsigned>(max(r1.steps, 0));
             }
             const int lmax = max(ok0 ? r0.steps : 0, ok1 ? r1.steps : 0);
@@ -372,9 +393,7 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
         if (i < A.n) {
             const uint64_t j = A.perm ? static_cast<uint64_t>(A.perm[i]) : i;
             const LaneOut r = MODE == kTableNone ? run_inline(A, j) : run_table<MODE>(A, tab, len, j, mask);
-            if (A.stop_distance) A.stop_distance[j] = r.x;
-            if (A.steps) A.steps[j] = r.steps;
-            if (A.hit_horizon) A.hit_horizon[j] = r.stopped ? 0 : 1;
+            store_out(A, j, r);
             const unsigned st = static_cast<unsigned>(max(r.steps, 0));
             my_steps += st;
             // lane-efficiency bookkeeping: the warp ran max(steps) slots per lane
@@ -475,7 +494,10 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(unsigned int* hist, int 
 }
 
 __global__ void __launch_bounds__(256) bin_scatter_kernel(const uint16_t* keys, uint64_t n,
-                                                          unsigned int* cursor, uint32_t* perm) {
+                                                          unsigned int* cursor, const double* v0,
+                                                          const double* floor_, const double* drag,
+                                                          const double* grade, PackedTerms* packed,
+                                                          uint32_t* inv_perm) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const unsigned lane = threadIdx.x & 31u;
     for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < n;
@@ -491,7 +513,25 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(const uint16_t* keys, 
         unsigned int start = 0;
         if (static_cast<int>(lane) == leader) start = atomicAdd(&cursor[key], __popc(peers));
         start = __shfl_sync(peers, start, leader);
-        perm[start + rank] = static_cast<uint32_t>(i);
+        const uint32_t pos = start + rank;
+        inv_perm[i] = pos;
+        // one aligned 32-byte record = one full sector: no read-for-fill
+        double2* dst = reinterpret_cast<double2*>(packed + pos);
+        dst[0] = make_double2(v0[i], floor_[i]);
+        dst[1] = make_double2(drag[i], grade[i]);
+    }
+}
+
+__global__ void __launch_bounds__(256) unpermute_kernel(const PackedOut* packed_out,
+                                                        const uint32_t* inv_perm, uint64_t n,
+                                                        double* d, int32_t* steps, uint8_t* hz) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+         j += stride) {
+        const PackedOut r = packed_out[inv_perm[j]];
+        if (d) d[j] = r.x;
+        if (steps) steps[j] = r.steps;
+        if (hz) hz[j] = static_cast<uint8_t>(r.hit_horizon);
     }
 }
 
@@ -616,13 +656,29 @@ cudaError_t launch_bin_scan(unsigned int* hist, int buckets, cudaStream_t s) {
 }
 
 cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* cursor,
-                               uint32_t* perm, cudaStream_t s) {
+                               const double* v0, const double* brake_floor, const double* drag,
+                               const double* grade, PackedTerms* packed, uint32_t* inv_perm,
+                               cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t blocks_needed = (n + 255) / 256;
     const int grid = static_cast<int>(std::min<uint64_t>(blocks_needed,
-                                                         static_cast<uint64_t>(sm_count(dev)) * 8));
-    bin_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, cursor, perm);
+                                                         static_cast<uint64_t>(sm_count_cached(dev)) * 8));
+    bin_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade, packed,
+                                            inv_perm);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpermute(const PackedOut* packed_out, const uint32_t* inv_perm, uint64_t n,
+                             double* stop_distance, int32_t* steps, uint8_t* hit_horizon,
+                             cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t blocks_needed = (n + 255) / 256;
+    const int grid = static_cast<int>(std::min<uint64_t>(blocks_needed,
+                                                         static_cast<uint64_t>(sm_count_cached(dev)) * 8));
+    unpermute_kernel<<<grid, 256, 0, s>>>(packed_out, inv_perm, n, stop_distance, steps,
+                                          hit_horizon);
     return cudaGetLastError();
 }
 

@@ -14,6 +14,19 @@ enum Schedule : int { kScheduleDefault = 0, kScheduleIndex = 1, kScheduleBinned 
 // Largest actuator table kept in shared memory (entries of 32 B).
 constexpr int kSmemTableMax = 6784;  // 217 KB of the 227 KB opt-in limit
 
+// Packed per-sample records used by the binned schedule: the binning
+// scatter writes each sample's inputs as one aligned 32-byte record in
+// sorted order (one full DRAM sector), the rollout reads and writes packed
+// records coalesced, and unpermute restores index order.
+struct __align__(32) PackedTerms {
+    double v0, brake_floor, drag, grade;
+};
+struct __align__(16) PackedOut {
+    double x;
+    int32_t steps;
+    uint32_t hit_horizon;
+};
+
 struct RolloutArgs {
     const double* v0;
     const double* brake_floor;
@@ -31,6 +44,8 @@ struct RolloutArgs {
     unsigned long long* total_steps;  // nullable
     unsigned int* work_counter;       // device, zeroed before launch
     unsigned long long* counters;     // nullable: [0] executed steps, [1] lane slots
+    const PackedTerms* packed_in;     // nullable: sorted packed inputs (binned schedule)
+    PackedOut* packed_out;            // nullable: sorted packed outputs (binned schedule)
 };
 
 struct PredictArgs {
@@ -65,8 +80,16 @@ cudaError_t launch_rollout(const RolloutArgs& a, int table_mode, int block_threa
 cudaError_t launch_predict(const PredictArgs& a, cudaStream_t s);
 cudaError_t launch_fp64_probe(double* out, int iters, uint64_t* ops, cudaStream_t s);
 cudaError_t launch_bin_scan(unsigned int* hist_to_cursor, int buckets, cudaStream_t s);
+// counting-sort scatter: inv_perm[i] = sorted slot of sample i, and the
+// sample's inputs are written packed into that slot
 cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* cursor,
-                               uint32_t* perm, cudaStream_t s);
+                               const double* v0, const double* brake_floor, const double* drag,
+                               const double* grade, PackedTerms* packed, uint32_t* inv_perm,
+                               cudaStream_t s);
+// outputs back to index order: out[j] = packed_out[inv_perm[j]]
+cudaError_t launch_unpermute(const PackedOut* packed_out, const uint32_t* inv_perm, uint64_t n,
+                             double* stop_distance, int32_t* steps, uint8_t* hit_horizon,
+                             cudaStream_t s);
 
 // statistics (bmc_stats.cu)
 struct StatsScratch {

@@ -286,6 +286,35 @@ class CudaExecutor:
                                                   _p(out), C.byref(cnt)))
         return out, int(cnt.value)
 
+    # mergeable building blocks (distributed.py) -------------------------
+    def partials(self, d, hz):
+        p = N.Partials()
+        self._check(self.lib.bmc_cuda_partials(self.ctx, C.c_void_p(d.data_ptr()),
+                                               C.c_void_p(hz.data_ptr()) if hz is not None else None,
+                                               int(d.numel()), C.byref(p)))
+        return {k: getattr(p, k) for k, _ in N.Partials._fields_ if k != "pad_"}
+
+    def moments(self, d, mean: float):
+        out = np.zeros(4)
+        self._check(self.lib.bmc_cuda_moments(self.ctx, C.c_void_p(d.data_ptr()), int(d.numel()),
+                                              mean, _p(out)))
+        return tuple(float(x) for x in out)
+
+    def histogram(self, d, origin: float, bin_width: float, bins: int) -> np.ndarray:
+        out = np.zeros(bins, dtype=np.uint64)
+        self._check(self.lib.bmc_cuda_histogram(self.ctx, C.c_void_p(d.data_ptr()), int(d.numel()),
+                                                origin, bin_width, bins, _p(out)))
+        return out
+
+    def select_pass(self, d, hz, exclude_horizon: bool, shift: int, prefixes) -> np.ndarray:
+        pre = np.ascontiguousarray(prefixes, dtype=np.uint64)
+        out = np.zeros((pre.shape[0], 256), dtype=np.uint64)
+        self._check(self.lib.bmc_cuda_select_pass(
+            self.ctx, C.c_void_p(d.data_ptr()),
+            C.c_void_p(hz.data_ptr()) if hz is not None else None, int(d.numel()),
+            1 if exclude_horizon else 0, shift, _p(pre), pre.shape[0], _p(out)))
+        return out
+
     def collision_probability(self, d, hz, headway: float) -> float:
         if not headway >= 0.0:
             raise N.ConfigError("risk.headway: must be >= 0")

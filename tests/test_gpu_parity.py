@@ -154,7 +154,7 @@ def test_device_resident_path(ref, executor):
     assert int(total.item()) == int(want["steps"].sum())
     rms, pms = executor.last_kernel_ms()
     assert rms > 0.0
-    assert executor.last_launches() == 4  # predict, scan, scatter, rollout
+    assert executor.last_launches() == 5  # predict, scan, scatter, rollout, unpermute
 
 
 def test_cpp_executor_api():

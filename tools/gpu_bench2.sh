@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python bench.py > gpurun_out/bench_1e8.log 2>&1
+echo "bench rc=$?" >> gpurun_out/bench_1e8.log
