@@ -9,6 +9,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -69,7 +70,11 @@ int ensure_table(bmc_ctx* ctx, const WorldDerived& d) {
         // Coarse brake_accel samples for the stop-step predictor: step
         // h = H*dt with H even, a(t) read at t = k*h/2 from the exact table.
         if (d.max_steps > 0 && d.dt > 0.0) {
-            const long long H = std::max<long long>(2, 2 * std::llround(0.025 / d.dt));
+            // coarse step ~0.1 s (BMC_COARSE_STEP_S overrides, for tuning):
+            // it only orders samples, never changes a result
+            double hs = 0.2;
+            if (const char* e = std::getenv("BMC_COARSE_STEP_S")) hs = std::max(1e-6, std::atof(e));
+            const long long H = std::max<long long>(2, 2 * std::llround(0.5 * hs / d.dt));
             const long long K = (d.max_steps + H - 1) / H;
             if (K <= kMaxCoarseSteps) {
                 std::vector<float> coarse(static_cast<size_t>(2 * K + 1));

@@ -440,18 +440,21 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictArgs P) {
         const float D = static_cast<float>(P.drag[i]);
         const float G = static_cast<float>(P.grade[i]);
         int pred = P.max_steps;
+        // scheduling only: FP32 with explicit FMAs (the file is -fmad=false)
+        const float nD = -D;
+        float b1 = fmaxf(s_a[0], F) - G;
         for (int k = 0; k < kmax; ++k) {
-            const float b1 = fmaxf(s_a[min(2 * k, last)], F);
-            const float b2 = fmaxf(s_a[min(2 * k + 1, last)], F);
-            const float b4 = fmaxf(s_a[min(2 * k + 2, last)], F);
-            const float k1 = b1 - D * v * v - G;
-            const float v2 = v + hh * k1;
-            const float k2 = b2 - D * v2 * v2 - G;
-            const float v3 = v + hh * k2;
-            const float k3 = b2 - D * v3 * v3 - G;
-            const float v4 = v + h * k3;
-            const float k4 = b4 - D * v4 * v4 - G;
-            const float vn = v + h6 * (k1 + 2.0f * k2 + 2.0f * k3 + k4);
+            const float b2 = fmaxf(s_a[min(2 * k + 1, last)], F) - G;
+            const float b4 = fmaxf(s_a[min(2 * k + 2, last)], F) - G;
+            const float k1 = __fmaf_rn(nD, v * v, b1);
+            const float v2 = __fmaf_rn(hh, k1, v);
+            const float k2 = __fmaf_rn(nD, v2 * v2, b2);
+            const float v3 = __fmaf_rn(hh, k2, v);
+            const float k3 = __fmaf_rn(nD, v3 * v3, b2);
+            const float v4 = __fmaf_rn(h, k3, v);
+            const float k4 = __fmaf_rn(nD, v4 * v4, b4);
+            const float vn = __fmaf_rn(h6, __fmaf_rn(2.0f, k2 + k3, k1 + k4), v);
+            b1 = b4;
             if (vn <= 0.0f) {
                 const float frac = v / (v - vn);
                 const float tstar = (static_cast<float>(k) + frac) * h;
@@ -498,27 +501,45 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(const uint16_t* keys, 
                                                           const double* floor_, const double* drag,
                                                           const double* grade, PackedTerms* packed,
                                                           uint32_t* inv_perm) {
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    const unsigned lane = threadIdx.x & 31u;
-    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < n;
-         base += stride) {
-        const uint64_t i = base + threadIdx.x;
-        const bool valid = i < n;
-        const unsigned active = __ballot_sync(0xffffffffu, valid);
-        if (!valid) continue;
-        const unsigned key = keys[i];
-        const unsigned peers = __match_any_sync(active, key);
-        const int leader = __ffs(peers) - 1;
-        const unsigned rank = __popc(peers & ((1u << lane) - 1u));
-        unsigned int start = 0;
-        if (static_cast<int>(lane) == leader) start = atomicAdd(&cursor[key], __popc(peers));
-        start = __shfl_sync(peers, start, leader);
-        const uint32_t pos = start + rank;
-        inv_perm[i] = pos;
-        // one aligned 32-byte record = one full sector: no read-for-fill
-        double2* dst = reinterpret_cast<double2*>(packed + pos);
-        dst[0] = make_double2(v0[i], floor_[i]);
-        dst[1] = make_double2(drag[i], grade[i]);
+    // Tile-aggregated counting-sort scatter: ranks inside a 2048-sample tile
+    // come from shared-memory atomics; each (tile, bucket) reserves its slots
+    // with ONE global atomic, so hot buckets are not serialised per warp.
+    constexpr int kItems = 8;
+    constexpr int kTile = 256 * kItems;
+    __shared__ unsigned int s_cnt[kMaxBuckets];
+    __shared__ unsigned int s_base[kMaxBuckets];
+    for (uint64_t tile = static_cast<uint64_t>(blockIdx.x) * kTile; tile < n;
+         tile += static_cast<uint64_t>(gridDim.x) * kTile) {
+        for (int b = threadIdx.x; b < kMaxBuckets; b += 256) s_cnt[b] = 0u;
+        __syncthreads();
+        unsigned key[kItems], rank[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            const uint64_t i = tile + static_cast<uint64_t>(k) * 256 + threadIdx.x;
+            if (i < n) {
+                key[k] = keys[i];
+                rank[k] = atomicAdd(&s_cnt[key[k]], 1u);
+            }
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < kMaxBuckets; b += 256) {
+            const unsigned c = s_cnt[b];
+            if (c) s_base[b] = atomicAdd(&cursor[b], c);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            const uint64_t i = tile + static_cast<uint64_t>(k) * 256 + threadIdx.x;
+            if (i < n) {
+                const uint32_t pos = s_base[key[k]] + rank[k];
+                inv_perm[i] = pos;
+                // one aligned 32-byte record = one full sector: no read-for-fill
+                double2* dst = reinterpret_cast<double2*>(packed + pos);
+                dst[0] = make_double2(v0[i], floor_[i]);
+                dst[1] = make_double2(drag[i], grade[i]);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -661,7 +682,7 @@ cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* c
                                cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint64_t blocks_needed = (n + 255) / 256;
+    const uint64_t blocks_needed = (n + 2047) / 2048;  // one 2048-sample tile per block pass
     const int grid = static_cast<int>(std::min<uint64_t>(blocks_needed,
                                                          static_cast<uint64_t>(sm_count_cached(dev)) * 8));
     bin_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade, packed,
