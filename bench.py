@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--seed", type=int, default=3)
     p.add_argument("--latency-reps", type=int, default=300)
     p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--ref-seconds", type=float, default=150.0)
     p.add_argument("--skip-e2e", action="store_true")
     p.add_argument("--skip-latency", action="store_true")
     p.add_argument("--skip-cpu", action="store_true")
@@ -123,7 +124,8 @@ def reference_arm(args, rank):
     probe, _ = ref.draw_batch(model, 2000)
     _, t_probe, _ = ref.run(probe, World(), "parallel", 0)
     per_sample = t_probe / 2000.0
-    budget = max(1.0, 150.0 / max(1, args.steps + args.warmup))  # whole run within minutes
+    # whole run within minutes: --ref-seconds of CPU work split over all steps
+    budget = max(0.05, args.ref_seconds / max(1, args.steps + args.warmup))
     n = int(min(args.samples, max(2000, budget / per_sample)))
     samples, _ = ref.draw_batch(model, n)
     for _ in range(args.warmup):
@@ -228,7 +230,7 @@ def feasibility_search(bmc, ex, sw, args):
             "path": "bmc_cuda_run_model (host sampler -> pinned SoA -> H2D, overlapped)"}
 
 
-def b200_arm(args, rank, world, local_rank, dist):
+def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     import torch
     import paper_2604_27193_b200 as bmc
 
@@ -262,7 +264,8 @@ def b200_arm(args, rank, world, local_rank, dist):
     kernel_ms = []
 
     from paper_2604_27193_b200 import distributed as D
-    coll = D.Collective(dist if world > 1 else None, f"cuda:{local_rank}")
+    cdev = coll_device or f"cuda:{local_rank}"
+    coll = D.Collective(dist if world > 1 else None, cdev)
 
     class CountingShard(D.DeviceShard):
         """DeviceShard that tallies the kernels each statistic launches."""
@@ -324,7 +327,7 @@ def b200_arm(args, rank, world, local_rank, dist):
         dist.barrier()
     clk = clocks.stop()
     elapsed_ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=f"cuda:{local_rank}")
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
@@ -356,7 +359,7 @@ def b200_arm(args, rank, world, local_rank, dist):
         for _ in range(reps):
             rep = ex.run(samples, sw, out=out)
         e2e_s = (time.perf_counter() - tt) / reps
-        te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local_rank}")
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=cdev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": n_total / float(te.item()), "unit": "rollouts/s",
@@ -420,6 +423,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("BMC_DIST_BACKEND", "nccl")  # gloo: multi-rank tests on one GPU
     if args.impl == "reference":
         reference_arm(args, rank)
         return
@@ -427,10 +431,14 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        local_rank = local_rank % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        else:
+            dist.init_process_group(backend)
     try:
-        b200_arm(args, rank, world, local_rank, dist)
+        b200_arm(args, rank, world, local_rank, dist, "cpu" if backend == "gloo" else None)
     finally:
         if dist is not None:
             dist.destroy_process_group()

@@ -23,6 +23,7 @@
 
 #include "brakemc/backends.hpp"
 #include "brakemc/errors.hpp"
+#include "brakemc/sampling.hpp"
 #include "brakemc_cuda.h"
 
 #include <chrono>
@@ -87,6 +88,26 @@ inline bmc_world world_of(const SimConfig& c, const VehicleGeometry& g, const Ph
                      p.gravity, p.air_density, p.frontal_area};
 }
 
+inline bmc_run_opts opts_of(const CudaExecOptions& o) {
+    bmc_run_opts r{};
+    r.schedule = o.schedule;
+    r.block_threads = o.block_threads;
+    r.table_mode = o.table_mode;
+    r.host_threads = o.host_threads;
+    r.chunk_samples = o.chunk_samples;
+    r.ilp = o.ilp;
+    return r;
+}
+
+inline bmc_model model_of(const UncertaintyModel& m) {
+    return bmc_model{m.seed,
+                     {m.initial_speed.mean, m.initial_speed.sd},
+                     {m.friction.mean, m.friction.sd},
+                     {m.grade.mean, m.grade.sd},
+                     {m.mass.mean, m.mass.sd},
+                     {m.drag_coeff.mean, m.drag_coeff.sd}};
+}
+
 }  // namespace cuda_detail
 
 /// Runs every sample on the selected B200s: contiguous index shards, one
@@ -115,13 +136,7 @@ inline ExecutionReport run_cuda(const SampleBatch& batch, const SimConfig& confi
     report.results.resize(batch.size());
 
     const bmc_world w = cuda_detail::world_of(config, geometry, constants);
-    bmc_run_opts opts{};
-    opts.schedule = options.schedule;
-    opts.block_threads = options.block_threads;
-    opts.table_mode = options.table_mode;
-    opts.host_threads = options.host_threads;
-    opts.chunk_samples = options.chunk_samples;
-    opts.ilp = options.ilp;
+    const bmc_run_opts opts = cuda_detail::opts_of(options);
 
     std::vector<bmc_ctx*> ctxs;
     for (int d : devices) ctxs.push_back(cuda_detail::context(d));

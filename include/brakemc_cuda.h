@@ -247,6 +247,13 @@ int bmc_cuda_select_pass(bmc_ctx* ctx, const double* stop_distance, const uint8_
                          size_t n, int exclude_horizon, int shift, const uint64_t* prefixes,
                          size_t m, uint64_t* hist);
 
+/* Device memory for callers without their own CUDA runtime (the C++
+ * CudaRun keeps results in HBM through these). */
+int bmc_cuda_alloc(bmc_ctx* ctx, size_t bytes, void** out);
+int bmc_cuda_free(bmc_ctx* ctx, void* ptr);
+int bmc_cuda_copy_to_host(bmc_ctx* ctx, void* host, const void* dev, size_t bytes);
+int bmc_cuda_copy_to_device(bmc_ctx* ctx, void* dev, const void* host, size_t bytes);
+
 /* ------------------------------------------------------- measurement */
 /* FP64 DADD/DMUL issue-rate probe (the rollout's roofline denominator;
  * MEASURED_PEAKS.json carries no FP64 entry).  Independent chains of

@@ -137,6 +137,10 @@ SIGNATURES = [
                                        C.POINTER(C.c_uint64)]),
     ("bmc_cuda_fp64_peak", C.c_int, [_P, C.c_int, C.POINTER(C.c_double),
                                      C.POINTER(C.c_double)]),
+    ("bmc_cuda_alloc", C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
+    ("bmc_cuda_free", C.c_int, [_P, _P]),
+    ("bmc_cuda_copy_to_host", C.c_int, [_P, _P, _P, C.c_size_t]),
+    ("bmc_cuda_copy_to_device", C.c_int, [_P, _P, _P, C.c_size_t]),
     ("bmc_cuda_partials", C.c_int, [_P, _P, _P, C.c_size_t, C.POINTER(Partials)]),
     ("bmc_cuda_moments", C.c_int, [_P, _P, C.c_size_t, C.c_double, _P]),
     ("bmc_cuda_histogram", C.c_int, [_P, _P, C.c_size_t, C.c_double, C.c_double, C.c_uint64,

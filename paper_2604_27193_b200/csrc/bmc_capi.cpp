@@ -549,6 +549,43 @@ int bmc_cuda_fp64_peak(bmc_ctx* ctx, int reps, double* ops_per_s, double* best_m
     return BMC_OK;
 }
 
+int bmc_cuda_alloc(bmc_ctx* ctx, size_t bytes, void** out) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    if (!out) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_alloc: null output");
+    *out = nullptr;
+    const cudaError_t e = cudaMalloc(out, bytes ? bytes : 1);
+    if (e != cudaSuccess) return fail(ctx, BMC_E_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return BMC_OK;
+}
+
+int bmc_cuda_free(bmc_ctx* ctx, void* ptr) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    if (ptr) BMC_CK(ctx, cudaFree(ptr));
+    return BMC_OK;
+}
+
+int bmc_cuda_copy_to_host(bmc_ctx* ctx, void* host, const void* dev, size_t bytes) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (bytes == 0) return BMC_OK;
+    BMC_CK(ctx, cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return BMC_OK;
+}
+
+int bmc_cuda_copy_to_device(bmc_ctx* ctx, void* dev, const void* host, size_t bytes) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (bytes == 0) return BMC_OK;
+    BMC_CK(ctx, cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return BMC_OK;
+}
+
 int bmc_cuda_last_launches(bmc_ctx* ctx, uint32_t* launches) {
     if (!ctx || !launches) return BMC_E_CONFIG;
     *launches = ctx->last_launches;

@@ -12,6 +12,7 @@
 // Exit 0 on success; prints one line per check.  Run by
 // tests/test_gpu_cpp.py on the GPU box.
 #include "brakemc/backends.hpp"
+#include "brakemc/cuda_analysis.hpp"
 #include "brakemc/cuda_executor.hpp"
 #include "brakemc/errors.hpp"
 #include "brakemc/sampling.hpp"
@@ -122,6 +123,81 @@ int main(int argc, char** argv) {
         all = all && verify_consistency(run_sequential(b, cfg, g2, phys), run_cuda(b, cfg, g2, phys)).pass;
         all = all && verify_consistency(run_sequential(b, c3, geo, phys), run_cuda(b, c3, geo, phys)).pass;
         check(all, "non-default SimConfig / geometry bit-exact");
+    }
+
+    // analysis.cpp on the device (CudaRun) vs the reference's host analysis
+    {
+        UncertaintyModel m;
+        m.seed = 3;
+        m.friction = NormalSpec{0.45, 0.20};
+        m.grade = NormalSpec{0.0, std::atan(0.06)};
+        const std::size_t n = quick ? 20000 : 60000;
+        const SampleBatch b = draw_batch(m, n);
+        const ExecutionReport ref = run_parallel(b, cfg, geo, phys, 0);
+        const CudaRun run = CudaRun::from_batch(b, cfg, geo, phys);
+        ExecutionReport back;
+        back.results = run.results();
+        check(verify_consistency(ref, back).pass, "CudaRun::from_batch results bit-exact");
+        const CudaRun streamed = CudaRun::from_model(m, n, cfg, geo, phys);
+        back.results = streamed.results();
+        check(verify_consistency(ref, back).pass && streamed.clamp_count() == b.clamp_count,
+              "CudaRun::from_model (streamed sampler) bit-exact, clamp count equal");
+
+        const DistributionSummary want = summarize(ref.results, 2.0);
+        const DistributionSummary got = run.summarize(2.0);
+        const auto rel = [](double a, double b) { return std::abs(a - b) <= 1e-12 * std::abs(b); };
+        check(got.n == want.n && got.horizon_count == want.horizon_count && got.min == want.min &&
+                  got.max == want.max && got.median == want.median &&
+                  got.histogram.origin == want.histogram.origin &&
+                  got.histogram.counts == want.histogram.counts &&
+                  got.right_skewed == want.right_skewed && rel(got.mean, want.mean) &&
+                  rel(got.sd, want.sd) && std::abs(got.skewness - want.skewness) <= 1e-9,
+              "summarize: counts/extrema/median/histogram exact, moments <= 1e-12 rel");
+
+        bool cp = true;
+        for (double h : {0.0, 50.0, 77.7, 120.0, 400.0, 1e9}) {
+            cp = cp && run.collision_probability(h) == collision_probability(ref.results, h);
+        }
+        check(cp, "collision_probability exact");
+        bool msh = true;
+        for (double r : {0.5, 0.3, 0.28, 0.05, 0.01, 0.001}) {
+            const double a = run.min_safe_headway(r), bref = min_safe_headway(ref.results, r);
+            msh = msh && (a == bref || (std::isinf(a) && std::isinf(bref)));
+        }
+        check(msh, "min_safe_headway exact (incl. +inf past the horizon tail)");
+        std::vector<double> grid = headway_grid(std::floor(want.min) - 5.0, 200.0, 1.0);
+        const RiskCurve rc_ref = build_risk_curve(ref.results, grid, {0.05, 0.01, 0.5}, 30.0);
+        const RiskCurve rc_gpu = run.build_risk_curve(grid, {0.05, 0.01, 0.5}, 30.0);
+        bool same = rc_ref.probabilities == rc_gpu.probabilities &&
+                    rc_ref.thresholds.size() == rc_gpu.thresholds.size();
+        for (std::size_t k = 0; same && k < rc_ref.thresholds.size(); ++k) {
+            same = rc_ref.thresholds[k].risk == rc_gpu.thresholds[k].risk &&
+                   rc_ref.thresholds[k].headway_m == rc_gpu.thresholds[k].headway_m &&
+                   rc_ref.thresholds[k].ttc_s == rc_gpu.thresholds[k].ttc_s;
+        }
+        check(same, "build_risk_curve exact");
+        const std::vector<std::size_t> nv{1000, 5000, 12000, n};
+        const auto cw = convergence_from_results(ref.results, nv, 12000);
+        const auto cg = run.convergence(nv, 12000);
+        bool conv = cw.size() == cg.size();
+        for (std::size_t k = 0; conv && k < cw.size(); ++k) {
+            conv = cw[k].n == cg[k].n && rel(cg[k].mean, cw[k].mean) && rel(cg[k].sd, cw[k].sd) &&
+                   std::abs(cg[k].delta_mean - cw[k].delta_mean) <= 1e-10 &&
+                   std::abs(cg[k].delta_sd - cw[k].delta_sd) <= 1e-10;
+        }
+        check(conv, "convergence rows (prefix mean/sd <= 1e-12 rel)");
+    }
+
+    // analysis.cpp:320-370 with the CUDA executor as the timed pipeline
+    {
+        FeasibilityOptions fo;
+        fo.search_cap = 1u << 16;  // bounded for the test
+        fo.timing_reps = 3;
+        const TimingReport tr = max_samples_within_budget_cuda(UncertaintyModel{}, cfg, geo, phys,
+                                                               TimingBudget{}, fo);
+        check(tr.max_samples == fo.search_cap && tr.capped && tr.meets_convergence_threshold &&
+                  tr.time_with_sampling_s < 0.53 && tr.sim_only_time_s <= tr.time_with_sampling_s,
+              "feasibility search on run_cuda (2^16 cap reached inside 530 ms)");
     }
 
     // backends.cpp:41-43: empty batch -> ConfigError with the field path

@@ -1,0 +1,74 @@
+"""bench.py contract checks (small sizes).
+
+CPU: the reference arm prints one JSON line with impl=reference.
+GPU: the B200 arm at N=1, and a 2-rank torchrun launch (gloo collectives,
+both ranks on cuda:0) exercising the sharded path the driver's scaling run
+uses with NCCL.
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = ["metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+        "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches"]
+
+
+def _json_lines(out: str):
+    return [json.loads(l) for l in out.splitlines() if l.startswith("{")]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_reference_arm_contract():
+    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
+                        "--warmup", "1", "--ref-seconds", "2"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=300)
+    assert p.returncode == 0, p.stderr
+    lines = _json_lines(p.stdout)
+    assert len(lines) == 1
+    line = lines[0]
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
+    for k in KEYS:
+        assert k in line, k
+
+
+@pytest.mark.gpu
+def test_b200_arm_single_gpu():
+    p = subprocess.run([sys.executable, "bench.py", "--samples", "3e5", "--steps", "2",
+                        "--warmup", "3", "--skip-cpu", "--latency-reps", "20"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    (line,) = _json_lines(p.stdout)
+    for k in KEYS + ["roofline", "clocks", "latency_25k", "feasibility_530ms"]:
+        assert k in line, k
+    assert line["value"] > 0 and line["gpu_launches"] > 0 and line["n_gpus"] == 1
+    assert line["roofline"]["bound"] == "fp64" and line["roofline"]["frac"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 32 * 300000
+
+
+@pytest.mark.gpu
+def test_b200_arm_two_ranks_gloo():
+    env = dict(os.environ, BMC_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
+           "--gpus", "2", "--samples", "2e5", "--steps", "2", "--warmup", "3", "--skip-cpu",
+           "--skip-latency"]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = _json_lines(p.stdout)
+    assert len(lines) == 1  # rank 0 only
+    assert lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0
+    assert lines[0]["config"]["parallelism"] == "shard2"
