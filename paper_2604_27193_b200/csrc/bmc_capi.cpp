@@ -115,11 +115,12 @@ int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uin
     int bt = opts.block_threads;
     if (bt == 0) bt = ilp == 2 ? kDefaultIlp2Block : (mode == kTableGlobal ? 256 : 1024);
     const bool ok_bt = ilp == 2 ? (bt == 512 || bt == 640 || bt == 768)
-                                : (bt == 256 || bt == 512 || bt == 768 || bt == 1024);
+                                : (bt == 256 || bt == 384 || bt == 512 || bt == 640 ||
+                                   bt == 768 || bt == 1024);
     if (!ok_bt) {
         return fail(ctx, BMC_E_CONFIG,
                     ilp == 2 ? "execution.block_threads: must be 512, 640 or 768 with ilp 2"
-                             : "execution.block_threads: must be 256, 512, 768 or 1024");
+                             : "execution.block_threads: must be 256, 384, 512, 640, 768 or 1024");
     }
     p.mode = mode;
     p.sched = sched;

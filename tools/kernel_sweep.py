@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--occupancy", action="store_true")
     a = ap.parse_args()
     n = int(a.samples)
     model = bmc.UncertaintyModel.mixed(3) if a.model == "mixed" else bmc.UncertaintyModel(seed=3)
@@ -50,6 +51,8 @@ def main():
         ["binned"], ["shared", "global"], [512, 640, 768])]
     if a.quick:
         configs = [c for c in configs if c[0] == "binned" and c[2] >= 512 and c[1] != "none"]
+    if a.occupancy:
+        configs = [("binned", t, b, 1) for t in ("shared", "global") for b in (384, 640, 1024)]
     for sched, table, bt, ilp in configs:
         if table == "none" and sched == "binned":
             continue
