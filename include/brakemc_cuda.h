@@ -40,7 +40,8 @@ enum {
     BMC_E_DOMAIN = -2,  /* friction_limit denominator <= 0 (domain_error) */
     BMC_E_CUDA = -3,    /* CUDA runtime / launch failure                  */
     BMC_E_NOMEM = -4,   /* host or device allocation failed               */
-    BMC_E_RANGE = -5    /* capacity exceeded (e.g. histogram buffer)      */
+    BMC_E_RANGE = -5,   /* capacity exceeded (e.g. histogram buffer)      */
+    BMC_E_IO = -6       /* file I/O / parse failure (IoError analogue)    */
 };
 
 /* == brakemc::ScenarioSample (dynamics.hpp:36-44), 40 bytes */
@@ -141,6 +142,13 @@ int bmc_draw_range(const bmc_model* model, uint64_t first, size_t n, bmc_sample*
 int bmc_stage_terms(const bmc_sample* samples, size_t n, const bmc_world* world,
                     double* initial_speed, double* brake_floor, double* drag_factor,
                     double* grade_accel, int threads);
+
+/* results.csv artifact (io.cpp:17-31 / 94-123): byte-identical writer
+ * ("%.17g", so doubles round-trip exactly) and reader; the reader rebuilds
+ * steps = llround(t_stop / dt) as cmd_verify does (cli.cpp:96-100). */
+int bmc_write_results_csv(const char* path, const bmc_result* results, size_t n, int threads);
+int bmc_read_results_csv(const char* path, double dt, bmc_result* out, size_t cap,
+                         size_t* n_out);
 
 /* ------------------------------------------------------------ executor */
 /* Drop-in core of brakemc::run_cuda: host AoS samples in, host AoS results

@@ -110,6 +110,9 @@ class Reference:
                                                    C.c_size_t, _D]
         L.ref_verify_consistency.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, _D, _U64,
                                              C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.ref_write_results_csv.argtypes = [C.c_void_p, C.c_size_t, C.c_char_p]
+        L.ref_read_results_csv.argtypes = [C.c_char_p, C.c_double, C.c_void_p, C.c_size_t,
+                                           C.POINTER(C.c_size_t)]
         L.ref_oracle_stopping_distance.restype = C.c_double
         L.ref_oracle_stopping_distance.argtypes = [_D, _D, C.c_double, C.c_double]
 
@@ -237,6 +240,18 @@ class Reference:
                                                     C.byref(first), C.byref(bw), C.byref(ok)))
         return dict(max_abs_deviation=float(dev.value), first_mismatch=int(first.value),
                     bitwise_equal=bool(bw.value), passed=bool(ok.value))
+
+    def write_results_csv(self, results, path: str):
+        results = np.ascontiguousarray(results, dtype=RESULT_DTYPE)
+        self._check(self.lib.ref_write_results_csv(_ptr(results), results.shape[0], path.encode()))
+
+    def read_results_csv(self, path: str, dt: float):
+        n = C.c_size_t(0)
+        self._check(self.lib.ref_read_results_csv(path.encode(), dt, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=RESULT_DTYPE)
+        self._check(self.lib.ref_read_results_csv(path.encode(), dt, _ptr(out), out.shape[0],
+                                                  C.byref(n)))
+        return out
 
     def oracle_stopping_distance(self, sample, world: World = World(), dt=1e-5, t_limit=30.0):
         s = np.array(list(sample), dtype=np.float64)

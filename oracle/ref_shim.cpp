@@ -11,9 +11,11 @@
 #include "brakemc/backends.hpp"
 #include "brakemc/errors.hpp"
 #include "brakemc/integrator.hpp"
+#include "brakemc/io.hpp"
 #include "brakemc/sampling.hpp"
 #include "oracles.hpp"
 
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -235,6 +237,22 @@ int ref_verify_consistency(const void* a, const void* b, std::size_t n, double* 
         *first_mismatch = v.first_mismatch;
         *bitwise_equal = v.bitwise_equal ? 1 : 0;
         *pass = v.pass ? 1 : 0;
+    });
+}
+
+// io.cpp:17-31 -- results.csv text, written verbatim to `path`
+int ref_write_results_csv(const void* results, std::size_t n, const char* path) {
+    return guarded([&] { write_text_file(path, results_csv(results_from(results, n))); });
+}
+
+// io.cpp:94-123 + cli.cpp:96-100 (steps rebuilt from t_stop / dt)
+int ref_read_results_csv(const char* path, double dt, void* out, std::size_t cap,
+                         std::size_t* n_out) {
+    return guarded([&] {
+        std::vector<RolloutResult> r = parse_results_csv(read_text_file(path));
+        for (RolloutResult& x : r) x.steps = std::llround(x.stop_time / dt);
+        *n_out = r.size();
+        if (r.size() <= cap && !r.empty()) std::memcpy(out, r.data(), r.size() * sizeof(RolloutResult));
     });
 }
 

@@ -13,7 +13,8 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "libbrakemc_b200.so")
 
-BMC_OK, BMC_E_CONFIG, BMC_E_DOMAIN, BMC_E_CUDA, BMC_E_NOMEM, BMC_E_RANGE = 0, -1, -2, -3, -4, -5
+BMC_OK, BMC_E_CONFIG, BMC_E_DOMAIN, BMC_E_CUDA, BMC_E_NOMEM, BMC_E_RANGE, BMC_E_IO = (
+    0, -1, -2, -3, -4, -5, -6)
 
 
 class BmcError(RuntimeError):
@@ -34,7 +35,13 @@ class CudaError(BmcError):
     code = BMC_E_CUDA
 
 
-_ERRORS = {BMC_E_CONFIG: ConfigError, BMC_E_DOMAIN: DomainError, BMC_E_CUDA: CudaError}
+class IoError(BmcError, OSError):
+    """brakemc::IoError analogue (errors.hpp:22-25)."""
+    code = BMC_E_IO
+
+
+_ERRORS = {BMC_E_CONFIG: ConfigError, BMC_E_DOMAIN: DomainError, BMC_E_CUDA: CudaError,
+           BMC_E_IO: IoError}
 
 
 class Sample(C.Structure):
@@ -113,6 +120,9 @@ SIGNATURES = [
     ("bmc_draw_range", C.c_int, [C.POINTER(Model), C.c_uint64, C.c_size_t, _P,
                                  C.POINTER(C.c_uint64), C.c_int]),
     ("bmc_stage_terms", C.c_int, [_P, C.c_size_t, C.POINTER(World), _P, _P, _P, _P, C.c_int]),
+    ("bmc_write_results_csv", C.c_int, [C.c_char_p, _P, C.c_size_t, C.c_int]),
+    ("bmc_read_results_csv", C.c_int, [C.c_char_p, C.c_double, _P, C.c_size_t,
+                                       C.POINTER(C.c_size_t)]),
     ("bmc_cuda_run", C.c_int, [_P, _P, C.c_size_t, C.POINTER(World), C.POINTER(RunOpts), _P,
                                C.POINTER(RunInfo)]),
     ("bmc_cuda_run_model", C.c_int, [_P, C.POINTER(Model), C.c_uint64, C.c_size_t,

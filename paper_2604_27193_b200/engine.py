@@ -102,6 +102,25 @@ def stage_terms(samples: np.ndarray, world: SimWorld = SimWorld(), threads: int 
     return out
 
 
+def write_results_csv(path: str, results: np.ndarray, threads: int = 0) -> None:
+    """results.csv (io.cpp:17-31), byte-identical to the reference writer."""
+    lib = N.load()
+    results = np.ascontiguousarray(results, dtype=RESULT_DTYPE)
+    N.check(lib.bmc_write_results_csv(path.encode(), _p(results), results.shape[0], threads))
+
+
+def read_results_csv(path: str, dt: float) -> np.ndarray:
+    """parse_results_csv (io.cpp:94-123) + steps = llround(t/dt) (cli.cpp:96-100)."""
+    lib = N.load()
+    n = C.c_size_t(0)
+    rc = lib.bmc_read_results_csv(path.encode(), dt, None, 0, C.byref(n))
+    if rc not in (N.BMC_OK, N.BMC_E_RANGE):
+        N.check(rc)
+    out = np.zeros(n.value, dtype=RESULT_DTYPE)
+    N.check(lib.bmc_read_results_csv(path.encode(), dt, _p(out), out.shape[0], C.byref(n)))
+    return out
+
+
 def device_count() -> int:
     lib = N.load()
     c = C.c_int(0)

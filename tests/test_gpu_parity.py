@@ -220,6 +220,19 @@ def test_graph_mode_decisions(ref, executor):
         g.close()
 
 
+def test_verify_against_csv_flow(ref, executor, tmp_path):
+    """cmd_verify --against (cli.cpp:82-116): CUDA results written as the
+    reference's results.csv, parsed by the reference, steps rebuilt, then
+    verify_consistency against run_sequential -> PASS."""
+    samples, _ = ref.draw_batch(Model(seed=3), 12000)
+    gpu = executor.run(samples).results
+    path = str(tmp_path / "results.csv")
+    bmc.engine.write_results_csv(path, gpu)
+    back = ref.read_results_csv(path, 0.001)
+    seq, _, _ = ref.run(samples, World(), "sequential")
+    assert_parity(ref, seq, back)
+
+
 def test_feasibility_search_logic():
     # analysis.cpp:258-318 with the reference test's synthetic linear machine
     # t(n) = 0.01 + 1e-6 n (test_analysis.cpp:235-266)

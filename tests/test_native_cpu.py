@@ -80,6 +80,28 @@ def test_stage_terms_domain_error():
         bmc.stage_terms(s, bmc.SimWorld(wheelbase=-0.1))
 
 
+def test_results_csv_matches_reference_io(ref, tmp_path):
+    """results.csv (io.cpp:17-31) byte-identical; parse (io.cpp:94-123) + step
+    rebuild (cli.cpp:96-100) round-trips every field bit for bit."""
+    from oracle.pyoracle import results_bitwise_equal
+    samples, _ = ref.draw_batch(Model.mixed(3), 2500)
+    res, _, _ = ref.run(samples, World(), "parallel")
+    mine, theirs = str(tmp_path / "mine.csv"), str(tmp_path / "ref.csv")
+    bmc.engine.write_results_csv(mine, res, threads=3)
+    ref.write_results_csv(res, theirs)
+    assert open(mine, "rb").read() == open(theirs, "rb").read()
+    assert results_bitwise_equal(bmc.engine.read_results_csv(theirs, 0.001), res)
+    assert results_bitwise_equal(ref.read_results_csv(mine, 0.001), res)
+    bad = tmp_path / "bad.csv"
+    bad.write_text("index,d,t,h\n0,1,2,0\n")
+    with pytest.raises(bmc.BmcError, match="unexpected header"):
+        bmc.engine.read_results_csv(str(bad), 0.001)
+    gap = tmp_path / "gap.csv"
+    gap.write_text("index,d_stop_m,t_stop_s,horizon_flag\n0,1,2,0\n2,1,2,0\n")
+    with pytest.raises(bmc.BmcError, match="non-contiguous"):
+        bmc.engine.read_results_csv(str(gap), 0.001)
+
+
 def test_no_cpu_fallback_without_device():
     if bmc.device_count() > 0:
         pytest.skip("a CUDA device is present")
