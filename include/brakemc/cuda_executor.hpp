@@ -174,4 +174,27 @@ inline const char* executor_name(ExecutorKind kind) {
     return kind == kCudaExecutorKind ? "cuda" : to_string(kind);
 }
 
+/// executor_from_string (run_config.cpp:107-115) extended with "cuda".
+/// Every other name keeps the reference's behaviour: "gpu" still throws
+/// (test_io_cli.cpp:103-104).
+inline ExecutorKind executor_from_string_with_cuda(const std::string& name) {
+    if (name == "sequential") return ExecutorKind::sequential;
+    if (name == "parallel") return ExecutorKind::parallel;
+    if (name == "cuda") return kCudaExecutorKind;
+    throw ConfigError("execution.executor", "must be \"sequential\", \"parallel\" or \"cuda\"");
+}
+
+/// run_configured_executor (cli.cpp:20-26) with the cuda branch.
+inline ExecutionReport run_executor(ExecutorKind kind, const SampleBatch& batch,
+                                    const SimConfig& config, const VehicleGeometry& geometry,
+                                    const PhysicalConstants& constants, unsigned workers = 0,
+                                    std::size_t chunk_size = 256,
+                                    const CudaExecOptions& cuda = {}) {
+    if (kind == kCudaExecutorKind) return run_cuda(batch, config, geometry, constants, cuda);
+    if (kind == ExecutorKind::sequential) {
+        return run_sequential(batch, config, geometry, constants);
+    }
+    return run_parallel(batch, config, geometry, constants, workers, chunk_size);
+}
+
 }  // namespace brakemc

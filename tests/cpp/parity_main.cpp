@@ -200,6 +200,24 @@ int main(int argc, char** argv) {
               "feasibility search on run_cuda (2^16 cap reached inside 530 ms)");
     }
 
+    // run_config.cpp:107-115 / cli.cpp:20-26 with the cuda branch
+    {
+        bool ok = executor_from_string_with_cuda("cuda") == kCudaExecutorKind &&
+                  executor_from_string_with_cuda("parallel") == ExecutorKind::parallel &&
+                  std::string(executor_name(kCudaExecutorKind)) == "cuda";
+        try {
+            executor_from_string_with_cuda("gpu");
+            ok = false;
+        } catch (const ConfigError& e) {
+            ok = ok && e.field() == "execution.executor";
+        }
+        const SampleBatch b = batch_of(11, 2000);
+        const ExecutionReport seq = run_executor(ExecutorKind::sequential, b, cfg, geo, phys);
+        const ExecutionReport gpu = run_executor(executor_from_string_with_cuda("cuda"), b, cfg, geo, phys);
+        check(ok && verify_consistency(seq, gpu).pass && gpu.executor == kCudaExecutorKind,
+              "executor selection: \"cuda\" dispatches to run_cuda, \"gpu\" still rejected");
+    }
+
     // backends.cpp:41-43: empty batch -> ConfigError with the field path
     {
         bool threw = false;
