@@ -1,0 +1,62 @@
+"""C5 upper range: 1e9 default-model samples on one B200, stats-only.
+
+Samples are drawn by the host pool straight into pinned SoA chunks
+(bmc_cuda_run_model), streamed H2D on a side stream while the previous
+chunk rolls out; per-sample outputs stay in HBM (13 GB at 1e9) and the
+statistics (summarize, 21-threshold TTC sweep, risk thresholds) run on the
+device.  No AoS batch or per-sample result ever exists on the host.
+
+python tools/run_1e9.py [--samples 1e9] [--chunk 16777216]
+Prints one JSON line.
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2604_27193_b200 as bmc  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--samples", type=float, default=1e9)
+    ap.add_argument("--chunk", type=int, default=1 << 24)
+    ap.add_argument("--seed", type=int, default=3)
+    a = ap.parse_args()
+    n = int(a.samples)
+    ex = bmc.CudaExecutor(0)
+    d = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = torch.empty(n, dtype=torch.int32, device="cuda")
+    hz = torch.empty(n, dtype=torch.uint8, device="cuda")
+    model = bmc.UncertaintyModel(seed=a.seed)
+    t0 = time.perf_counter()
+    rep, clamps = ex.run_model(model, n, device_out=(d, st, hz), chunk=a.chunk)
+    t_roll = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    summ = ex.summarize(d, hz, 2.0)
+    ttc = [1.0 + 0.25 * k for k in range(21)]
+    counts = ex.exceedance_counts(d, hz, [t * 30.0 for t in ttc])
+    heads = ex.min_safe_headways(d, hz, [0.05, 0.01, 0.001, 1e-4, 1e-5])
+    t_stats = time.perf_counter() - t1
+    print(json.dumps({
+        "samples": n, "seed": a.seed, "chunk": a.chunk, "clamp_count": clamps,
+        "pipeline_s": t_roll, "rollouts_per_s_with_sampling": n / t_roll,
+        "rollout_kernel_ms_total": rep.kernel_ms, "kernel_rollouts_per_s": n / (rep.kernel_ms * 1e-3),
+        "total_rk4_steps": rep.total_steps, "chunks": rep.chunks,
+        "stats_s": t_stats,
+        "summary": {k: v for k, v in summ.items() if k != "histogram"},
+        "ttc_thresholds_s": ttc, "exceedance_counts": [int(c) for c in counts],
+        "min_safe_headway_m": dict(zip(["0.05", "0.01", "0.001", "1e-4", "1e-5"], heads)),
+        "host_cores": os.cpu_count(),
+    }, default=float))
+
+
+if __name__ == "__main__":
+    main()
