@@ -181,8 +181,9 @@ def realtime(bmc, ex, sw, args):
     g = ex.graph(n, sw)
     try:
         batches = [bmc.draw_batch(bmc.UncertaintyModel(seed=s), n)[0] for s in range(1, 17)]
-        for b in batches[:4]:
-            g.run(b)
+        for _ in range(2):
+            for b in batches:
+                g.run(b)
         sim_ms, full_ms, steps = [], [], []
         for k in range(args.latency_reps):
             t1 = time.perf_counter()
