@@ -200,6 +200,18 @@ int main(int argc, char** argv) {
               "feasibility search on run_cuda (2^16 cap reached inside 530 ms)");
     }
 
+    // multi-device sharding path (one host thread + context per entry); on a
+    // single-GPU box the same device twice exercises the threading/slicing
+    {
+        const SampleBatch b = batch_of(21, 30001, true);
+        const ExecutionReport seq = run_parallel(b, cfg, geo, phys, 0);
+        CudaExecOptions o;
+        o.devices = {0, 0, 0};
+        const ExecutionReport gpu = run_cuda(b, cfg, geo, phys, o);
+        check(verify_consistency(seq, gpu).pass && gpu.worker_count == 3,
+              "run_cuda with 3 shards (threads) bit-exact, worker_count = shards");
+    }
+
     // run_config.cpp:107-115 / cli.cpp:20-26 with the cuda branch
     {
         bool ok = executor_from_string_with_cuda("cuda") == kCudaExecutorKind &&
