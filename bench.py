@@ -17,6 +17,11 @@ L2, so no flush is needed), device-timed with CUDA events on the engine's
 stream, max over ranks.  `e2e`: the same rollouts through bmc_cuda_run (the
 run_cuda core) from pageable host samples to host results, H2D/D2H inside.
 Sample generation is excluded from both (backends.hpp:22-24), and reported.
+`device_sampler`: the same shard drawn on the GPU by the op-for-op glibc port
+(csrc/bmc_libm.h), checked bit for bit against the host-drawn terms over the
+whole shard, and `e2e_model`: model -> host results through
+bmc_cuda_run_model with the device sampler (sampling included, the
+convention of the reference's feasibility search, analysis.cpp:331-338).
 """
 import argparse
 import json
@@ -184,6 +189,7 @@ def realtime(bmc, ex, sw, args):
         for _ in range(2):
             for b in batches:
                 g.run(b)
+            g.run_model(bmc.UncertaintyModel(seed=999))  # first call captures its graph
         sim_ms, full_ms, steps = [], [], []
         for k in range(args.latency_reps):
             t1 = time.perf_counter()
@@ -195,6 +201,9 @@ def realtime(bmc, ex, sw, args):
             g.run_model(bmc.UncertaintyModel(seed=1000 + k))
             full_ms.append(1e3 * (time.perf_counter() - t1))
         return {"samples": n, "budget_ms": 530.0, "mode": "CUDA graph (H2D, bin, rollout, D2H)",
+                "with_sampling_mode": "CUDA graph (%s)" % (
+                    "device sampler: params H2D, draw, bin, rollout, D2H"
+                    if bmc.device_sampler_available() else "host sampler, terms H2D"),
                 "sim_only_ms": {"p50": _pct(sim_ms, 50), "p99": _pct(sim_ms, 99),
                                 "reps": len(sim_ms)},
                 "with_sampling_ms": {"p50": _pct(full_ms, 50), "p99": _pct(full_ms, 99),
@@ -203,6 +212,46 @@ def realtime(bmc, ex, sw, args):
                 "kernel_launches_per_decision": rep.launches}
     finally:
         g.close()
+
+
+def device_sampler(bmc, ex, sw, args, model, n, begin, dev_terms, world, dist, cdev):
+    """Draw the rank's shard on the device and prove it equals the host draw
+    (all 4 x n terms, bitwise); time the draw kernel and the model-driven
+    end-to-end path (sampling included)."""
+    import torch
+    if not bmc.device_sampler_available():
+        return {"available": False,
+                "why": bmc.load().bmc_last_error().decode(errors="replace")}
+    ex.draw_device(model, min(n, 1 << 20), first=begin, world=sw, samples=False)  # warm-up
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    terms, _, dclamps = ex.draw_device(model, n, first=begin, world=sw, samples=False)
+    draw_s = time.perf_counter() - t
+    same = all(torch.equal(terms[i].view(torch.int64), dev_terms[i].view(torch.int64))
+               for i in range(4))
+    del terms
+    torch.cuda.empty_cache()
+    out = np.empty(n, dtype=bmc.RESULT_DTYPE)
+    ex.run_model(model, n, first=begin, world=sw, out=out, sampler="device")  # warm-up
+    if world > 1:
+        dist.barrier()
+    reps = max(1, min(args.steps, 3))
+    tt = time.perf_counter()
+    for _ in range(reps):
+        rep, _ = ex.run_model(model, n, first=begin, world=sw, out=out, sampler="device")
+    e2e_s = (time.perf_counter() - tt) / reps
+    te = torch.tensor([e2e_s, 0.0 if same else 1.0], dtype=torch.float64, device=cdev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    return {"available": True, "bit_identical_to_host_draw": float(te[1].item()) == 0.0,
+            "verified_samples": n, "clamp_count": dclamps, "draw_s": draw_s,
+            "draw_samples_per_s": n / draw_s,
+            "e2e_model": {"value": int(args.samples) / float(te[0].item()), "unit": "rollouts/s",
+                          "h2d_bytes_per_step": rep.h2d_bytes,
+                          "d2h_bytes_per_step": rep.d2h_bytes, "reps": reps,
+                          "path": "bmc_cuda_run_model(sampler=device): UncertaintyModel -> "
+                                  "device draw + RolloutTerms -> bin+rollout -> D2H -> AoS "
+                                  "results (sampling included)"}}
 
 
 def feasibility_search(bmc, ex, sw, args):
@@ -228,7 +277,9 @@ def feasibility_search(bmc, ex, sw, args):
     return {"budget_ms": 530.0, "max_samples": n_max, "capped": capped,
             "search_cap": 1 << 27, "time_with_sampling_ms": with_s * 1e3 if with_s else None,
             "meets_convergence_threshold": n_max >= 12000,
-            "path": "bmc_cuda_run_model (host sampler -> pinned SoA -> H2D, overlapped)"}
+            "path": "bmc_cuda_run_model (%s)" % (
+                "device sampler: draw + rollout on the GPU" if bmc.device_sampler_available()
+                else "host sampler -> pinned SoA -> H2D, overlapped")}
 
 
 def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
@@ -370,6 +421,11 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
                "reps": reps}
         del out
 
+    # ---- on-device sampler: bit-identity over the shard + sampling-included e2e
+    dsamp = None
+    if not args.skip_e2e:
+        dsamp = device_sampler(bmc, ex, sw, args, model, n, begin, dev_terms, world, dist, cdev)
+
     # ---- real-time decision batch (C2): 25k samples, p50/p99 over replays
     latency = None
     feasibility = None
@@ -409,6 +465,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
                                         "(MEASURED_PEAKS.json has no FP64 entry)",
                          "spec_peak_tflops": SPEC_FP64_OPS / 1e12},
             "e2e": e2e,
+            "device_sampler": dsamp,
             "latency_25k": latency,
             "feasibility_530ms": feasibility,
             "cpu_baseline": cpu,

@@ -50,6 +50,7 @@ struct CudaExecOptions {
     int block_threads = 0;        ///< 0 default (timing only)
     int table_mode = 0;           ///< 0 auto (timing only)
     int ilp = 0;                  ///< samples per thread, 0 default (timing only)
+    int sampler = 0;              ///< model-driven runs: 0 auto, 1 host pool, 2 device (timing only)
 };
 
 static_assert(sizeof(ScenarioSample) == sizeof(bmc_sample), "ScenarioSample layout");
@@ -96,6 +97,7 @@ inline bmc_run_opts opts_of(const CudaExecOptions& o) {
     r.host_threads = o.host_threads;
     r.chunk_samples = o.chunk_samples;
     r.ilp = o.ilp;
+    r.sampler = o.sampler;
     return r;
 }
 

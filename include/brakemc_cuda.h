@@ -105,7 +105,8 @@ typedef struct {
     int32_t host_threads;   /* 0 = all hardware threads (host staging / unpack) */
     uint64_t chunk_samples; /* 0 = default pipeline chunk for bmc_cuda_run */
     int32_t ilp;            /* samples per thread: 0 = default, 1, or 2 (table modes) */
-    int32_t reserved_;
+    int32_t sampler;        /* model-driven runs: 0 = auto (device when bmc_device_sampler_available),
+                               1 = host pool, 2 = device (BMC_E_CONFIG when unavailable) */
 } bmc_run_opts;
 
 /* Timing breakdown of one bmc_cuda_run call (seconds). */
@@ -142,6 +143,28 @@ int bmc_draw_range(const bmc_model* model, uint64_t first, size_t n, bmc_sample*
 int bmc_stage_terms(const bmc_sample* samples, size_t n, const bmc_world* world,
                     double* initial_speed, double* brake_floor, double* drag_factor,
                     double* grade_accel, int threads);
+
+/* On-device sampler gate.  The device sampler replays glibc 2.39's FMA
+ * libm variants (__log_fma, __cos_fma, __sin_fma) op for op; it is
+ * bit-identical to bmc_draw_range only on a host whose own libm is that
+ * variant.  bmc_libm_selftest compares the port against the live host libm
+ * over n sampler draws (+ every branch boundary); mismatches[7] =
+ * {log, log near 1, cos(2 pi u), sin |x|<=1.5, sin/cos reduced, normal
+ * deviate, boundaries/range}.  BMC_OK iff all are zero.
+ * bmc_device_sampler_available caches a quick check for the process. */
+int bmc_libm_selftest(uint64_t n, uint64_t seed, int threads, uint64_t* mismatches);
+int bmc_device_sampler_available(int* available);
+
+/* On-device draw_batch (sampling.cpp:67-100) of samples [first, first+n),
+ * fused with RolloutTerms::from (dynamics.cpp:57-68): bit-identical to
+ * bmc_draw_range + bmc_stage_terms when bmc_device_sampler_available.
+ * terms: device, 4*n doubles laid out [v0 | brake_floor | drag_factor |
+ * grade_accel] (nullable); samples: device AoS (nullable).  Synchronous;
+ * BMC_E_DOMAIN for a non-positive friction_limit denominator, BMC_E_RANGE if
+ * an argument left the ported glibc range. */
+int bmc_cuda_draw_device(bmc_ctx* ctx, const bmc_model* model, uint64_t first, size_t n,
+                         const bmc_world* world, double* terms, bmc_sample* samples,
+                         uint64_t* clamp_count);
 
 /* results.csv artifact (io.cpp:17-31 / 94-123): byte-identical writer
  * ("%.17g", so doubles round-trip exactly) and reader; the reader rebuilds

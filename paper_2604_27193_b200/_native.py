@@ -81,7 +81,7 @@ class Outputs(C.Structure):
 class RunOpts(C.Structure):
     _fields_ = [("schedule", C.c_int32), ("block_threads", C.c_int32), ("table_mode", C.c_int32),
                 ("host_threads", C.c_int32), ("chunk_samples", C.c_uint64), ("ilp", C.c_int32),
-                ("reserved_", C.c_int32)]
+                ("sampler", C.c_int32)]
 
 
 class RunInfo(C.Structure):
@@ -120,6 +120,10 @@ SIGNATURES = [
     ("bmc_draw_range", C.c_int, [C.POINTER(Model), C.c_uint64, C.c_size_t, _P,
                                  C.POINTER(C.c_uint64), C.c_int]),
     ("bmc_stage_terms", C.c_int, [_P, C.c_size_t, C.POINTER(World), _P, _P, _P, _P, C.c_int]),
+    ("bmc_libm_selftest", C.c_int, [C.c_uint64, C.c_uint64, C.c_int, _P]),
+    ("bmc_device_sampler_available", C.c_int, [C.POINTER(C.c_int)]),
+    ("bmc_cuda_draw_device", C.c_int, [_P, C.POINTER(Model), C.c_uint64, C.c_size_t,
+                                       C.POINTER(World), _P, _P, C.POINTER(C.c_uint64)]),
     ("bmc_write_results_csv", C.c_int, [C.c_char_p, _P, C.c_size_t, C.c_int]),
     ("bmc_read_results_csv", C.c_int, [C.c_char_p, C.c_double, _P, C.c_size_t,
                                        C.POINTER(C.c_size_t)]),

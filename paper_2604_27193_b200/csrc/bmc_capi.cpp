@@ -232,6 +232,55 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
     return BMC_OK;
 }
 
+
+int use_device_sampler(bmc_ctx* ctx, const bmc_run_opts& o, bool* device) {
+    *device = false;
+    if (o.sampler < 0 || o.sampler > 2) {
+        return fail(ctx, BMC_E_CONFIG, "execution.sampler: must be 0 (auto), 1 (host) or 2 (device)");
+    }
+    if (o.sampler == 1) return BMC_OK;
+    std::string why;
+    const bool ok = device_sampler_supported(&why);
+    if (!ok && o.sampler == 2) return fail(ctx, BMC_E_CONFIG, "execution.sampler: " + why);
+    *device = ok;
+    return BMC_OK;
+}
+
+DrawArgs draw_args(const bmc_model& m, uint64_t first, uint64_t n, const bmc_world& w) {
+    DrawArgs a{};
+    a.seed = m.seed;
+    a.spec[0] = m.initial_speed;
+    a.spec[1] = m.friction;
+    a.spec[2] = m.grade;
+    a.spec[3] = m.mass;
+    a.spec[4] = m.drag_coeff;
+    a.first = first;
+    a.n = n;
+    a.cg_height = w.cg_height;
+    a.wheelbase = w.wheelbase;
+    a.gravity = w.gravity;
+    a.air_density = w.air_density;
+    a.frontal_area = w.frontal_area;
+    return a;
+}
+
+int finish_draw(bmc_ctx* ctx, const DevBuf& ctr, uint64_t* clamps) {
+    unsigned long long c[2] = {0, 0};
+    BMC_CK(ctx, cudaMemcpyAsync(c, ctr.p, sizeof c, cudaMemcpyDeviceToHost, ctx->stream));
+    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    const unsigned flags = static_cast<unsigned>(c[1]);
+    if (flags & kDrawDomain) {
+        return fail(ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
+    }
+    if (flags & kDrawUnported) {
+        return fail(ctx, BMC_E_RANGE,
+                    "device sampler: a libm argument left the ported glibc range (log of x <= 0 "
+                    "or subnormal, |x| >= 105414350 or non-finite for sin/cos)");
+    }
+    if (clamps) *clamps = c[0];
+    return BMC_OK;
+}
+
 namespace {
 
 // Chunked host<->device pipeline (2 slots): per chunk the host pool fills
@@ -249,8 +298,14 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
     Plan plan;
     int rc = make_plan(ctx, d, o, chunk, &plan);
     if (rc != BMC_OK) return rc;
+    bool dev_draw = false;
+    if (model && (rc = use_device_sampler(ctx, o, &dev_draw)) != BMC_OK) return rc;
+    if (dev_draw) {
+        BMC_CK(ctx, ctx->draw_ctr.reserve(16));
+        BMC_CK(ctx, cudaMemsetAsync(ctx->draw_ctr.p, 0, 16, ctx->stream));
+    }
     for (auto& s : ctx->slots) {
-        BMC_CK(ctx, s.h_terms.reserve(chunk * 32));
+        if (!dev_draw) BMC_CK(ctx, s.h_terms.reserve(chunk * 32));
         BMC_CK(ctx, s.d_terms.reserve(chunk * 32));
         if (host_out) {
             BMC_CK(ctx, s.h_out.reserve(chunk * 13));
@@ -309,35 +364,49 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
         if ((rc = finish(s)) != BMC_OK) return rc;
         s.offset = k * chunk;
         s.len = std::min<uint64_t>(chunk, n - s.offset);
-        double* hv0 = s.h_terms.as<double>();
-        double* hfl = hv0 + s.len;
-        double* hdr = hfl + s.len;
-        double* hgr = hdr + s.len;
-        std::atomic<int> status{BMC_OK};
-        host_pool().parallel_for(
-            s.len,
-            [&](size_t b, size_t e) {
-                int r;
-                if (samples) {
-                    r = stage_terms_serial(samples + s.offset + b, e - b, w, hv0 + b, hfl + b,
-                                           hdr + b, hgr + b);
-                } else {
-                    uint64_t c = 0;
-                    r = draw_terms_serial(*model, first + s.offset + b, e - b, w, hv0 + b, hfl + b,
-                                          hdr + b, hgr + b, &c);
-                    clamps += c;
-                }
-                if (r != BMC_OK) status = r;
-            },
-            threads);
-        if (status != BMC_OK) {
-            cudaStreamSynchronize(ctx->stream);
-            cudaStreamSynchronize(ctx->d2h);
-            return fail(ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
+        if (dev_draw) {
+            // samples drawn on the device straight into this slot's terms
+            DrawArgs da = draw_args(*model, first + s.offset, s.len, w);
+            double* dt0 = s.d_terms.as<double>();
+            da.v0 = dt0;
+            da.brake_floor = dt0 + s.len;
+            da.drag = dt0 + 2 * s.len;
+            da.grade = dt0 + 3 * s.len;
+            da.clamps = ctx->draw_ctr.as<unsigned long long>();
+            da.flags = reinterpret_cast<unsigned int*>(ctx->draw_ctr.as<char>() + 8);
+            BMC_CK(ctx, launch_draw_terms(da, ctx->sms, ctx->stream));
+            ++launches;
+        } else {
+            double* hv0 = s.h_terms.as<double>();
+            double* hfl = hv0 + s.len;
+            double* hdr = hfl + s.len;
+            double* hgr = hdr + s.len;
+            std::atomic<int> status{BMC_OK};
+            host_pool().parallel_for(
+                s.len,
+                [&](size_t b, size_t e) {
+                    int r;
+                    if (samples) {
+                        r = stage_terms_serial(samples + s.offset + b, e - b, w, hv0 + b, hfl + b,
+                                               hdr + b, hgr + b);
+                    } else {
+                        uint64_t c = 0;
+                        r = draw_terms_serial(*model, first + s.offset + b, e - b, w, hv0 + b, hfl + b,
+                                              hdr + b, hgr + b, &c);
+                        clamps += c;
+                    }
+                    if (r != BMC_OK) status = r;
+                },
+                threads);
+            if (status != BMC_OK) {
+                cudaStreamSynchronize(ctx->stream);
+                cudaStreamSynchronize(ctx->d2h);
+                return fail(ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
+            }
+            BMC_CK(ctx, cudaMemcpyAsync(s.d_terms.p, s.h_terms.p, s.len * 32, cudaMemcpyHostToDevice, ctx->h2d));
+            BMC_CK(ctx, cudaEventRecord(s.h2d_done, ctx->h2d));
+            BMC_CK(ctx, cudaStreamWaitEvent(ctx->stream, s.h2d_done, 0));
         }
-        BMC_CK(ctx, cudaMemcpyAsync(s.d_terms.p, s.h_terms.p, s.len * 32, cudaMemcpyHostToDevice, ctx->h2d));
-        BMC_CK(ctx, cudaEventRecord(s.h2d_done, ctx->h2d));
-        BMC_CK(ctx, cudaStreamWaitEvent(ctx->stream, s.h2d_done, 0));
         const double* dv0 = s.d_terms.as<double>();
         const bmc_terms terms{dv0, dv0 + s.len, dv0 + 2 * s.len, dv0 + 3 * s.len};
         bmc_outputs outs;
@@ -369,15 +438,17 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
     }
     unsigned long long steps_total = 0;
     BMC_CK(ctx, cudaMemcpy(&steps_total, ctx->total_steps.p, sizeof steps_total, cudaMemcpyDeviceToHost));
+    uint64_t dev_clamps = 0;
+    if (dev_draw && (rc = finish_draw(ctx, ctx->draw_ctr, &dev_clamps)) != BMC_OK) return rc;
     const double wall = std::chrono::duration<double>(Clock::now() - t0).count();
     ctx->last_launches = launches;
-    if (clamp_count) *clamp_count = clamps.load();
+    if (clamp_count) *clamp_count = dev_draw ? dev_clamps : clamps.load();
     if (info) {
         info->wall_s = wall;
         info->kernel_ms = kernel_ms;
         info->predict_ms = predict_ms;
         info->total_steps = steps_total;
-        info->h2d_bytes = n * 32;
+        info->h2d_bytes = dev_draw ? 0 : n * 32;
         info->d2h_bytes = host_out ? n * 13 : 0;
         info->launches = launches;
         info->chunks = static_cast<uint32_t>(nchunks);
@@ -460,7 +531,7 @@ void bmc_cuda_destroy(bmc_ctx* ctx) {
         if (s.d2h_done) cudaEventDestroy(s.d2h_done);
         s.kev.destroy();
     }
-    for (bmc::DevBuf* b : {&ctx->d_table, &ctx->d_coarse, &ctx->total_steps, &ctx->partials,
+    for (bmc::DevBuf* b : {&ctx->d_table, &ctx->d_coarse, &ctx->total_steps, &ctx->draw_ctr, &ctx->partials,
                            &ctx->sel_hist, &ctx->sel_pref, &ctx->sorted_h, &ctx->buckets,
                            &ctx->hist_buf}) {
         b->release();
@@ -585,6 +656,35 @@ int bmc_cuda_copy_to_device(bmc_ctx* ctx, void* dev, const void* host, size_t by
     BMC_CK(ctx, cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
     BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
     return BMC_OK;
+}
+
+int bmc_cuda_draw_device(bmc_ctx* ctx, const bmc_model* model, uint64_t first, size_t n,
+                         const bmc_world* world, double* terms, bmc_sample* samples,
+                         uint64_t* clamp_count) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (n == 0) return fail(ctx, BMC_E_CONFIG, "samples: must be >= 1");  // sampling.cpp:68-70
+    if (!model || !world) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_draw_device: null argument");
+    bmc_run_opts o{};
+    o.sampler = 2;
+    bool dev = false;
+    if ((rc = bmc::use_device_sampler(ctx, o, &dev)) != BMC_OK) return rc;
+    bmc::DrawArgs a = bmc::draw_args(*model, first, n, *world);
+    if (terms) {
+        a.v0 = terms;
+        a.brake_floor = terms + n;
+        a.drag = terms + 2 * n;
+        a.grade = terms + 3 * n;
+    }
+    a.samples = reinterpret_cast<double*>(samples);
+    BMC_CK(ctx, ctx->draw_ctr.reserve(16));
+    BMC_CK(ctx, cudaMemsetAsync(ctx->draw_ctr.p, 0, 16, ctx->stream));
+    a.clamps = ctx->draw_ctr.as<unsigned long long>();
+    a.flags = reinterpret_cast<unsigned int*>(ctx->draw_ctr.as<char>() + 8);
+    BMC_CK(ctx, bmc::launch_draw_terms(a, ctx->sms, ctx->stream));
+    ctx->last_launches = 1;
+    return bmc::finish_draw(ctx, ctx->draw_ctr, clamp_count);
 }
 
 int bmc_cuda_last_launches(bmc_ctx* ctx, uint32_t* launches) {

@@ -135,6 +135,7 @@ struct bmc_ctx {
 
     bmc::Scratch scratch;
     bmc::DevBuf total_steps;
+    bmc::DevBuf draw_ctr;  // device sampler: u64 clamp count + u32 flags
     uint32_t last_launches = 0;
 
     bmc::Slot slots[2];
@@ -171,6 +172,13 @@ int ensure_table(bmc_ctx* ctx, const WorldDerived& d);
 int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uint64_t n,
               Plan* plan);
 int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n);
+// Device sampler (bmc_capi.cpp): resolve bmc_run_opts.sampler to a yes/no.
+int use_device_sampler(bmc_ctx* ctx, const bmc_run_opts& o, bool* device);
+// Fill DrawArgs from a model + world (no output pointers set).
+DrawArgs draw_args(const bmc_model& m, uint64_t first, uint64_t n, const bmc_world& w);
+// Read back + reset the draw counters; maps flags to BMC_E_DOMAIN/RANGE.
+int finish_draw(bmc_ctx* ctx, const DevBuf& ctr, uint64_t* clamps);
+bool device_sampler_supported(std::string* why);  // bmc_libm_check.cpp
 // Enqueue predictor/binning (when planned) + rollout on `s`.  ev may be
 // null (no timing events, e.g. under stream capture).
 int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms& terms,

@@ -26,6 +26,15 @@ struct bmc_graph {
     cudaEvent_t done = nullptr;
     unsigned threads = 1;
     uint32_t launches = 0;
+    // Model-driven decisions on the device sampler: a second graph
+    // {H2D draw params, draw kernel, rollout, D2H outputs + draw counters},
+    // captured on the first bmc_cuda_graph_run_model call.
+    int sampler = 0;  // bmc_run_opts.sampler
+    cudaGraph_t mgraph = nullptr;
+    cudaGraphExec_t mexec = nullptr;
+    bmc::DevBuf d_dyn, d_ctr;
+    bmc::PinBuf h_dyn, h_ctr;
+    uint32_t mlaunches = 0;
 };
 
 namespace {
@@ -33,6 +42,11 @@ namespace {
 void release(bmc_graph* g) {
     if (g->exec) cudaGraphExecDestroy(g->exec);
     if (g->graph) cudaGraphDestroy(g->graph);
+    if (g->mexec) cudaGraphExecDestroy(g->mexec);
+    if (g->mgraph) cudaGraphDestroy(g->mgraph);
+    for (bmc::DevBuf* b : {&g->d_dyn, &g->d_ctr}) b->release();
+    g->h_dyn.release();
+    g->h_ctr.release();
     if (g->done) cudaEventDestroy(g->done);
     g->sc.release();
     for (bmc::DevBuf* b : {&g->table, &g->coarse, &g->d_terms, &g->d_out, &g->steps_total}) b->release();
@@ -52,11 +66,11 @@ int graph_fail(bmc_graph* g, int code, const std::string& msg) {
                               std::string(#expr) + ": " + cudaGetErrorString(e_));       \
     } while (0)
 
-// Replay + unpack; the caller has filled g->h_terms.
+// Replay + unpack; the caller has filled g->h_terms (or g->h_dyn).
 int replay(bmc_graph* g, bmc_result* out, bmc_run_info* info,
-           std::chrono::steady_clock::time_point t0) {
+           std::chrono::steady_clock::time_point t0, bool model_graph = false) {
     bmc_ctx* ctx = g->ctx;
-    BMC_GK(g, cudaGraphLaunch(g->exec, ctx->stream));
+    BMC_GK(g, cudaGraphLaunch(model_graph ? g->mexec : g->exec, ctx->stream));
     BMC_GK(g, cudaEventRecord(g->done, ctx->stream));
     BMC_GK(g, cudaEventSynchronize(g->done));
     const size_t n = g->n;
@@ -81,14 +95,67 @@ int replay(bmc_graph* g, bmc_result* out, bmc_run_info* info,
     if (info) {
         std::memset(info, 0, sizeof *info);
         info->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        info->h2d_bytes = n * 32;
-        info->d2h_bytes = n * 13;
-        info->launches = g->launches;
+        info->h2d_bytes = model_graph ? sizeof(bmc::DrawDyn) : n * 32;
+        info->d2h_bytes = n * 13 + (model_graph ? 16 : 0);
+        info->launches = model_graph ? g->mlaunches : g->launches;
         info->chunks = 1;
         unsigned long long steps = 0;
         BMC_GK(g, cudaMemcpy(&steps, g->steps_total.p, sizeof steps, cudaMemcpyDeviceToHost));
         info->total_steps = steps;
     }
+    return BMC_OK;
+}
+
+// Capture the device-sampler decision graph (lazily, first model decision).
+int capture_model_graph(bmc_graph* g) {
+    bmc_ctx* ctx = g->ctx;
+    const size_t n = g->n;
+    BMC_CK(ctx, g->d_dyn.reserve(sizeof(bmc::DrawDyn)));
+    BMC_CK(ctx, g->h_dyn.reserve(sizeof(bmc::DrawDyn)));
+    BMC_CK(ctx, g->d_ctr.reserve(16));
+    BMC_CK(ctx, g->h_ctr.reserve(16));
+    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    bmc_model zero{};
+    bmc::DrawArgs da = bmc::draw_args(zero, 0, n, g->world);
+    double* dv0 = g->d_terms.as<double>();
+    da.v0 = dv0;
+    da.brake_floor = dv0 + n;
+    da.drag = dv0 + 2 * n;
+    da.grade = dv0 + 3 * n;
+    da.clamps = g->d_ctr.as<unsigned long long>();
+    da.flags = reinterpret_cast<unsigned int*>(g->d_ctr.as<char>() + 8);
+    da.dyn = g->d_dyn.as<bmc::DrawDyn>();
+    const bmc_terms terms{dv0, dv0 + n, dv0 + 2 * n, dv0 + 3 * n};
+    char* dout = g->d_out.as<char>();
+    const bmc_outputs outs{reinterpret_cast<double*>(dout), reinterpret_cast<int32_t*>(dout + n * 8),
+                           reinterpret_cast<uint8_t*>(dout + n * 12)};
+    cudaStream_t s = ctx->stream;
+    BMC_CK(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    uint32_t launches = 1;
+    bool ok = cudaMemcpyAsync(g->d_dyn.p, g->h_dyn.p, sizeof(bmc::DrawDyn), cudaMemcpyHostToDevice, s) == cudaSuccess &&
+              cudaMemsetAsync(g->d_ctr.p, 0, 16, s) == cudaSuccess &&
+              cudaMemsetAsync(g->steps_total.p, 0, sizeof(unsigned long long), s) == cudaSuccess &&
+              bmc::launch_draw_terms(da, ctx->sms, s) == cudaSuccess;
+    if (ok) {
+        ok = bmc::enqueue_rollout(ctx, g->plan, g->sc, terms, n, outs,
+                                  g->steps_total.as<unsigned long long>(), s, nullptr,
+                                  &launches) == BMC_OK;
+    }
+    if (ok) ok = cudaMemcpyAsync(g->h_out.p, g->d_out.p, n * 13, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+                 cudaMemcpyAsync(g->h_ctr.p, g->d_ctr.p, 16, cudaMemcpyDeviceToHost, s) == cudaSuccess;
+    const cudaError_t ec = cudaStreamEndCapture(s, &g->mgraph);
+    if (!ok || ec != cudaSuccess) {
+        const std::string why = ctx->err.empty() ? cudaGetErrorString(ec) : ctx->err;
+        if (g->mgraph) cudaGraphDestroy(g->mgraph);
+        g->mgraph = nullptr;
+        return bmc::fail(ctx, BMC_E_CUDA, "graph capture failed: " + why);
+    }
+    const cudaError_t ei = cudaGraphInstantiate(&g->mexec, g->mgraph, 0);
+    if (ei != cudaSuccess) {
+        g->mexec = nullptr;
+        return bmc::fail(ctx, BMC_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ei));
+    }
+    g->mlaunches = launches;
     return BMC_OK;
 }
 
@@ -112,6 +179,7 @@ int bmc_cuda_graph_create(bmc_ctx* ctx, size_t n, const bmc_world* world,
     if ((rc = bmc::derive_world(*world, &g->d, &err)) != BMC_OK) return bmc::fail(ctx, rc, err);
     const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
     g->threads = bmc::resolve_threads(o.host_threads);
+    g->sampler = o.sampler;
     if ((rc = bmc::make_plan(ctx, g->d, o, n, &g->plan)) != BMC_OK) return rc;
     // private copies of the world-dependent tables
     if (g->plan.table_len > 0 && g->plan.table) {
@@ -196,6 +264,32 @@ int bmc_cuda_graph_run_model(bmc_graph* g, const bmc_model* model, uint64_t firs
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(g->ctx->mu);
     const auto t0 = std::chrono::steady_clock::now();
+    bmc_run_opts o{};
+    o.sampler = g->sampler;
+    bool dev = false;
+    if ((rc = bmc::use_device_sampler(g->ctx, o, &dev)) != BMC_OK) return rc;
+    if (dev) {
+        if (!g->mexec && (rc = capture_model_graph(g)) != BMC_OK) return rc;
+        bmc::DrawDyn* p = g->h_dyn.as<bmc::DrawDyn>();
+        p->seed = model->seed;
+        p->spec[0] = model->initial_speed;
+        p->spec[1] = model->friction;
+        p->spec[2] = model->grade;
+        p->spec[3] = model->mass;
+        p->spec[4] = model->drag_coeff;
+        p->first = first;
+        if ((rc = replay(g, out, info, t0, true)) != BMC_OK) return rc;
+        const unsigned long long* c = g->h_ctr.as<unsigned long long>();
+        const unsigned flags = static_cast<unsigned>(c[1]);
+        if (flags & bmc::kDrawDomain) {
+            return bmc::fail(g->ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
+        }
+        if (flags & bmc::kDrawUnported) {
+            return bmc::fail(g->ctx, BMC_E_RANGE, "device sampler: a libm argument left the ported glibc range");
+        }
+        if (clamp_count) *clamp_count = c[0];
+        return BMC_OK;
+    }
     const size_t n = g->n;
     double* h = g->h_terms.as<double>();
     std::atomic<int> status{BMC_OK};

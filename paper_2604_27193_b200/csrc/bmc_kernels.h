@@ -66,6 +66,33 @@ struct PredictArgs {
     unsigned int* hist;     // out: per-bucket counts (zeroed before launch)
 };
 
+// On-device sampler (bmc_sampler.cu): samples [first, first+n) of
+// draw_batch(model, .) and their RolloutTerms, bit-identical to the host
+// producers through the glibc port (bmc_libm.h).
+enum DrawFlags : unsigned { kDrawDomain = 1u, kDrawUnported = 2u };
+// Per-launch draw parameters read from device memory (CUDA-graph replays
+// update them with a captured H2D copy instead of re-capturing).
+struct DrawDyn {
+    uint64_t seed;
+    bmc_normal spec[5];
+    uint64_t first;
+};
+struct DrawArgs {
+    uint64_t seed;
+    bmc_normal spec[5];    // v0, mu, theta, m, c_d (UncertaintyModel order)
+    uint64_t first, n;
+    double cg_height, wheelbase, gravity, air_density, frontal_area;
+    double* v0;            // nullable (then no terms are formed)
+    double* brake_floor;
+    double* drag;
+    double* grade;
+    double* samples;       // nullable: AoS bmc_sample records (5 doubles)
+    unsigned long long* clamps;  // device, accumulated
+    unsigned int* flags;         // device, DrawFlags OR-ed
+    const DrawDyn* dyn;          // nullable: overrides seed/spec/first
+};
+cudaError_t launch_draw_terms(const DrawArgs& a, int sms, cudaStream_t s);
+
 struct LaunchShape {
     int block_threads;
     int grid;

@@ -28,6 +28,8 @@ RESULT_DTYPE = np.dtype(
 # schedule / table modes (bmc_run_opts)
 SCHEDULE = {"default": 0, "index": 1, "binned": 2}
 TABLE = {"auto": 0, "shared": 1, "global": 2, "none": 3}
+# model-driven sampler (bmc_run_opts.sampler)
+SAMPLER = {"auto": 0, "host": 1, "device": 2}
 
 
 @dataclass
@@ -121,6 +123,22 @@ def read_results_csv(path: str, dt: float) -> np.ndarray:
     return out
 
 
+def libm_selftest(n: int = 1 << 20, seed: int = 12345, threads: int = 0) -> np.ndarray:
+    """Compare the glibc port (csrc/bmc_libm.h) with the live host libm; returns
+    the 7 mismatch counters (all zero on a matching host, see brakemc_cuda.h)."""
+    lib = N.load()
+    out = np.zeros(7, dtype=np.uint64)
+    lib.bmc_libm_selftest(n, seed, threads, _p(out))
+    return out
+
+
+def device_sampler_available() -> bool:
+    lib = N.load()
+    v = C.c_int(0)
+    N.check(lib.bmc_device_sampler_available(C.byref(v)))
+    return bool(v.value)
+
+
 def device_count() -> int:
     lib = N.load()
     c = C.c_int(0)
@@ -169,9 +187,10 @@ class CudaExecutor:
         N.check(rc, self.ctx)
 
     @staticmethod
-    def _opts(schedule="default", block_threads=0, table="auto", host_threads=0, chunk=0, ilp=0):
+    def _opts(schedule="default", block_threads=0, table="auto", host_threads=0, chunk=0, ilp=0,
+              sampler="auto"):
         return N.RunOpts(SCHEDULE[schedule], block_threads, TABLE[table], host_threads, chunk,
-                         ilp, 0)
+                         ilp, SAMPLER[sampler])
 
     # -------------------------------------------------------------- executor
     def run(self, samples: np.ndarray, world: SimWorld = SimWorld(), out: np.ndarray = None,
@@ -221,6 +240,26 @@ class CudaExecutor:
                         int(info.total_steps), int(info.h2d_bytes), int(info.d2h_bytes),
                         int(info.launches), int(info.chunks))
         return rep, int(clamps.value)
+
+    def draw_device(self, model: UncertaintyModel, n: int, first: int = 0,
+                    world: SimWorld = SimWorld(), terms: bool = True, samples: bool = True):
+        """On-device draw_batch (sampling.cpp:67-100) + RolloutTerms::from
+        (dynamics.cpp:57-68) through the glibc port: returns (terms, samples,
+        clamp_count) with terms a (4, n) float64 CUDA tensor [v0, floor, drag,
+        grade] and samples an (n, 5) float64 CUDA tensor (ScenarioSample
+        field order), each None when not requested."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        t = torch.empty((4, n), dtype=torch.float64, device=dev) if terms else None
+        smp = torch.empty((n, 5), dtype=torch.float64, device=dev) if samples else None
+        w = world.c()
+        m = model.c()
+        clamps = C.c_uint64(0)
+        self._check(self.lib.bmc_cuda_draw_device(
+            self.ctx, C.byref(m), first, n, C.byref(w),
+            C.c_void_p(t.data_ptr()) if t is not None else None,
+            C.c_void_p(smp.data_ptr()) if smp is not None else None, C.byref(clamps)))
+        return t, smp, int(clamps.value)
 
     def graph(self, n: int, world: SimWorld = SimWorld(), **opts) -> "DecisionGraph":
         """Capture the real-time decision batch of size n as a CUDA graph."""

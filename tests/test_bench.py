@@ -57,6 +57,9 @@ def test_b200_arm_single_gpu():
     assert line["value"] > 0 and line["gpu_launches"] > 0 and line["n_gpus"] == 1
     assert line["roofline"]["bound"] == "fp64" and line["roofline"]["frac"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 32 * 300000
+    ds = line["device_sampler"]
+    assert ds["available"] and ds["bit_identical_to_host_draw"] and ds["verified_samples"] == 300000
+    assert ds["e2e_model"]["h2d_bytes_per_step"] == 0 and ds["e2e_model"]["value"] > 0
 
 
 @pytest.mark.gpu
@@ -72,3 +75,4 @@ def test_b200_arm_two_ranks_gloo():
     assert len(lines) == 1  # rank 0 only
     assert lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0
     assert lines[0]["config"]["parallelism"] == "shard2"
+    assert lines[0]["device_sampler"]["bit_identical_to_host_draw"]

@@ -1,0 +1,198 @@
+#!/usr/bin/env python
+"""BASELINE.json configs C1, C3 and C4 on one B200 next to the reference CPU
+path, on the same box and the same samples (C2 and C5 live in bench.py and
+tools/run_1e9.py).
+
+C1  reference baseline scenario: default model (dry asphalt, flat-road mean
+    grade 0), seed 3, 10k samples, dt = 1e-3 -- the reference's run_sequential
+    and run_parallel vs run_cuda, parity checked (verify_consistency).
+C3  sample-count sweep 1k .. 1M (the paper's scaling study): wall time per
+    call for run_cuda (host samples -> host results), the model-driven path
+    with the device sampler (sampling included) and the reference's
+    run_parallel on all host threads; median of 5 (backends.cpp:161-181;
+    fewer CPU reps at the large sizes), and the reference's timing fit
+    t = overhead + slope * n (fit_timing_model, backends.cpp:129-159).
+C4  mixed-condition, divergence-heavy: wet/icy friction N(0.45, 0.2^2),
+    grade +-6 %, 1e6 samples: device-resident rollout time,
+    SIMT lane efficiency, horizon share, and the TTC-threshold sweep
+    T in {1.0, 1.25, ..., 6.0} s (headway T * 30 m/s) whose counts must equal
+    the reference's collision_probability(results, T * v) * n exactly.
+
+python tools/configs.py [--out profiles/round1_configs.json] [--quick]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2604_27193_b200 as bmc  # noqa: E402
+from oracle.pyoracle import Model, Reference, World  # noqa: E402
+
+
+def median_time(fn, reps, warmup=1):
+    for _ in range(warmup):
+        fn()
+    ts = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t)
+    return statistics.median(ts)
+
+
+def median_ref(fn, reps, warmup=1):
+    """The reference's own wall_time_s (execution only, backends.hpp:22-24)."""
+    for _ in range(warmup):
+        fn()
+    return statistics.median([fn()[1] for _ in range(reps)])
+
+
+def fit(ns, ts):
+    """fit_timing_model (backends.cpp:129-159): OLS t = overhead + slope * n."""
+    x = np.asarray(ns, dtype=np.float64)
+    y = np.asarray(ts, dtype=np.float64)
+    xm, ym = x.mean(), y.mean()
+    slope = float(((x - xm) * (y - ym)).sum() / ((x - xm) ** 2).sum())
+    return {"overhead_ms": 1e3 * (ym - slope * xm), "slope_ns_per_sample": 1e9 * slope,
+            "asymptotic_rollouts_per_s": 1.0 / slope if slope > 0 else None}
+
+
+def to_model(m: Model) -> bmc.UncertaintyModel:
+    return bmc.UncertaintyModel(m.seed, *zip(m.mean, m.sd))
+
+
+def c1(ref, ex):
+    m = Model(seed=3)
+    n = 10000
+    samples, _ = ref.draw_batch(m, n)
+    seq, t_seq, _ = ref.run(samples, World(), "sequential")
+    par, t_par, wc = ref.run(samples, World(), "parallel", 0)
+    t_seq = median_ref(lambda: ref.run(samples, World(), "sequential"), 5)
+    t_par = median_ref(lambda: ref.run(samples, World(), "parallel", 0), 5)
+    out = np.empty(n, dtype=bmc.RESULT_DTYPE)
+    t_gpu = median_time(lambda: ex.run(samples, out=out), 5)
+    v = ref.verify_consistency(seq, out)
+    t_draw = median_time(lambda: ref.draw_batch(m, n), 5)
+    t_model = median_time(lambda: ex.run_model(to_model(m), n, out=out, sampler="device"), 5)
+    v2 = ref.verify_consistency(seq, out)
+    s = ref.summarize(seq)
+    return {
+        "samples": n, "model": "default (seed 3)", "host_threads": wc,
+        "reference_run_sequential_s": t_seq, "reference_run_parallel_s": t_par,
+        "reference_draw_batch_s": t_draw,
+        "run_cuda_s": t_gpu, "run_cuda_parity": v,
+        "run_model_device_sampler_s": t_model, "run_model_parity": v2,
+        "speedup_vs_sequential": t_seq / t_gpu, "speedup_vs_parallel": t_par / t_gpu,
+        "speedup_with_sampling_vs_parallel": (t_par + t_draw) / t_model,
+        "reference_summary": {k: s[k] for k in ("mean", "sd", "min", "max", "median")},
+    }
+
+
+def c3(ref, ex, quick):
+    m = Model(seed=3)
+    sizes = [1000, 2000, 5000, 10000, 25000, 50000, 100000, 250000, 500000, 1000000]
+    if quick:
+        sizes = sizes[:6]
+    full, _ = ref.draw_batch(m, sizes[-1])
+    rows = []
+    out = np.empty(sizes[-1], dtype=bmc.RESULT_DTYPE)
+    for n in sizes:
+        s = full[:n]
+        o = out[:n]
+        t_gpu = median_time(lambda: ex.run(s, out=o), 5)
+        t_mod = median_time(lambda: ex.run_model(to_model(m), n, out=o, sampler="device"), 5)
+        reps = 5 if n <= 50000 else (3 if n <= 250000 else 1)
+        t_cpu = median_ref(lambda: ref.run(s, World(), "parallel", 0), reps,
+                           warmup=1 if n <= 250000 else 0)
+        rows.append({"samples": n, "run_cuda_s": t_gpu, "run_model_device_sampler_s": t_mod,
+                     "reference_run_parallel_s": t_cpu, "cpu_reps": reps,
+                     "run_cuda_rollouts_per_s": n / t_gpu,
+                     "reference_rollouts_per_s": n / t_cpu, "speedup": t_cpu / t_gpu})
+        print(f"  C3 n={n:>8}: gpu {t_gpu*1e3:8.3f} ms  model {t_mod*1e3:8.3f} ms  "
+              f"cpu {t_cpu*1e3:9.1f} ms  x{t_cpu/t_gpu:8.1f}", file=sys.stderr, flush=True)
+    ns = [r["samples"] for r in rows]
+    return {"model": "default (seed 3)", "rows": rows,
+            "fit_run_cuda": fit(ns, [r["run_cuda_s"] for r in rows]),
+            "fit_run_model_device_sampler": fit(ns, [r["run_model_device_sampler_s"] for r in rows]),
+            "fit_reference_run_parallel": fit(ns, [r["reference_run_parallel_s"] for r in rows])}
+
+
+def c4(ref, ex, quick):
+    import torch
+    m = Model.mixed(3)
+    n = 200000 if quick else 1000000
+    terms, samples, clamps = ex.draw_device(to_model(m), n)
+    d = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = torch.empty(n, dtype=torch.int32, device="cuda")
+    hz = torch.empty(n, dtype=torch.uint8, device="cuda")
+    total = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tl = [terms[i] for i in range(4)]
+    ex.rollout_device(tl, (d, st, hz), total_steps=total)  # warm-up
+    ms = []
+    for _ in range(5):
+        total.zero_()
+        ex.rollout_device(tl, (d, st, hz), total_steps=total)
+        ms.append(ex.last_kernel_ms()[0])
+    steps, slots, eff = ex.lane_efficiency()
+    ttc = [1.0 + 0.25 * k for k in range(21)]
+    v_close = 30.0
+    heads = [t * v_close for t in ttc]
+    counts = ex.exceedance_counts(d, hz, heads)
+    # parity: the reference on the same samples, collision_probability per threshold
+    host = samples.cpu().numpy().view(bmc.SAMPLE_DTYPE).reshape(n)
+    k = min(n, 200000)
+    want, t_cpu, wc = ref.run(np.ascontiguousarray(host[:k]), World(), "parallel", 0)
+    got_d = d[:k].cpu().numpy()
+    same = bool(np.array_equal(got_d.view(np.uint64), want["stop_distance"].view(np.uint64)))
+    sub_counts = ex.exceedance_counts(d[:k], hz[:k], heads)
+    ref_counts = [int(round(ref.collision_probability(want, h) * k)) for h in heads]
+    kms = statistics.median(ms)
+    total_steps = int(total.item())
+    return {
+        "model": "mixed (seed 3): mu ~ N(0.45, 0.2^2), grade ~ N(0, atan(0.06)^2)",
+        "samples": n, "clamp_count": clamps,
+        "horizon_share": float(hz.float().mean().item()),
+        "mean_steps": total_steps / n,
+        "rollout_kernel_ms": kms, "rollouts_per_s_kernel": n / (kms * 1e-3),
+        "lane_efficiency": eff,
+        "executed_fp64_tflops": 32 * total_steps / (kms * 1e-3) / 1e12,
+        "ttc_thresholds_s": ttc, "closing_speed_mps": v_close,
+        "exceedance_counts": [int(c) for c in counts],
+        "collision_probability": [int(c) / n for c in counts],
+        "parity_subset": k, "parity_stop_distance_bitwise": same,
+        "parity_counts_equal_reference": [int(c) for c in sub_counts] == ref_counts,
+        "reference_run_parallel_rollouts_per_s": k / t_cpu, "host_threads": wc,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--quick", action="store_true")
+    a = ap.parse_args()
+    ref = Reference()
+    ex = bmc.CudaExecutor(0)
+    res = {"host_threads": ref.hardware_concurrency(),
+           "device_sampler": bmc.device_sampler_available()}
+    t = time.time()
+    res["C1"] = c1(ref, ex)
+    res["C3"] = c3(ref, ex, a.quick)
+    res["C4"] = c4(ref, ex, a.quick)
+    res["wall_s"] = time.time() - t
+    line = json.dumps(res, default=float)
+    print(line)
+    if a.out:
+        with open(a.out, "w") as f:
+            f.write(json.dumps(res, default=float, indent=1) + "\n")
+    ex.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,12 +1,14 @@
 """C5 upper range: 1e9 default-model samples on one B200, stats-only.
 
-Samples are drawn by the host pool straight into pinned SoA chunks
-(bmc_cuda_run_model), streamed H2D on a side stream while the previous
-chunk rolls out; per-sample outputs stay in HBM (13 GB at 1e9) and the
+Samples are drawn on the device by the glibc-port sampler (--sampler device,
+the default when the host libm passes the gate) or by the host pool straight
+into pinned SoA chunks streamed H2D on a side stream (--sampler host), while
+the previous chunk rolls out (bmc_cuda_run_model); per-sample outputs stay in
+HBM (13 GB at 1e9) and the
 statistics (summarize, 21-threshold TTC sweep, risk thresholds) run on the
 device.  No AoS batch or per-sample result ever exists on the host.
 
-python tools/run_1e9.py [--samples 1e9] [--chunk 16777216]
+python tools/run_1e9.py [--samples 1e9] [--chunk 16777216] [--sampler auto|host|device]
 Prints one JSON line.
 """
 import argparse
@@ -29,6 +31,7 @@ def main():
     ap.add_argument("--samples", type=float, default=1e9)
     ap.add_argument("--chunk", type=int, default=1 << 24)
     ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--sampler", default="auto", choices=["auto", "host", "device"])
     a = ap.parse_args()
     n = int(a.samples)
     ex = bmc.CudaExecutor(0)
@@ -37,7 +40,7 @@ def main():
     hz = torch.empty(n, dtype=torch.uint8, device="cuda")
     model = bmc.UncertaintyModel(seed=a.seed)
     t0 = time.perf_counter()
-    rep, clamps = ex.run_model(model, n, device_out=(d, st, hz), chunk=a.chunk)
+    rep, clamps = ex.run_model(model, n, device_out=(d, st, hz), chunk=a.chunk, sampler=a.sampler)
     t_roll = time.perf_counter() - t0
     t1 = time.perf_counter()
     summ = ex.summarize(d, hz, 2.0)
@@ -47,6 +50,7 @@ def main():
     t_stats = time.perf_counter() - t1
     print(json.dumps({
         "samples": n, "seed": a.seed, "chunk": a.chunk, "clamp_count": clamps,
+        "sampler": "device" if rep.h2d_bytes == 0 else "host", "h2d_bytes": rep.h2d_bytes,
         "pipeline_s": t_roll, "rollouts_per_s_with_sampling": n / t_roll,
         "rollout_kernel_ms_total": rep.kernel_ms, "kernel_rollouts_per_s": n / (rep.kernel_ms * 1e-3),
         "total_rk4_steps": rep.total_steps, "chunks": rep.chunks,
