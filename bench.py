@@ -386,14 +386,14 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     value = n_total / (ms_per_step * 1e-3)
 
     roll_ms = sum(kernel_ms) / len(kernel_ms)
-    traffic = None
+    traffic, traffic_detail = None, None
     tpath = os.path.join(ROOT, "profiles", "rollout_traffic.json")
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
-        traffic = {"bytes_per_launch": tj["bytes_per_sample"] * n,
-                   "bytes_per_sample": tj["bytes_per_sample"],
-                   "algorithmic_bytes_per_sample": tj["algorithmic_bytes_per_sample"],
-                   "source": tj["source"] + ", scaled to this launch's sample count"}
+        traffic = tj["bytes_per_sample"] * n  # DRAM bytes per launch (ncu), this launch's n
+        traffic_detail = {"bytes_per_sample": tj["bytes_per_sample"],
+                          "algorithmic_bytes_per_sample": tj["algorithmic_bytes_per_sample"],
+                          "source": tj["source"] + ", scaled to this launch's sample count"}
     steps_per_launch = steps_sum / args.steps
     achieved = ALGO_FLOPS_PER_STEP * steps_per_launch / (roll_ms * 1e-3)
     executed = EXEC_FLOPS_PER_STEP * steps_per_launch / (roll_ms * 1e-3)
@@ -456,6 +456,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
                        "sampling_s": sample_s, "clamp_count": clamps},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
                          "unit": "TFLOP/s", "frac": achieved / peak_ops, "traffic": traffic,
+                         "traffic_detail": traffic_detail,
                          "kernel": "rollout_kernel", "kernel_ms": roll_ms,
                          "rk4_steps_per_launch": steps_per_launch,
                          "algorithmic_flops_per_step": ALGO_FLOPS_PER_STEP,

@@ -20,6 +20,7 @@
 // warp's 32 lanes retire within a few steps of each other; warps pull
 // 32-sample groups longest-first from a global counter (persistent CTAs).
 #include "bmc_kernels.h"
+#include "bmc_rk4.cuh"
 
 #include <cub/block/block_scan.cuh>
 
@@ -29,36 +30,6 @@ namespace bmc {
 namespace {
 
 int sm_count_cached(int device);
-
-__device__ __forceinline__ double clamp_brake(double a, double floor_) {
-    // dynamics.hpp:82-84 (ternary semantics, not fmax)
-    return a > floor_ ? a : floor_;
-}
-
-// longitudinal_accel (dynamics.hpp:115-118): (braking - D*(v*v)) - G
-__device__ __forceinline__ double accel(double braking, double v, double D, double G) {
-    return __dsub_rn(__dsub_rn(braking, __dmul_rn(D, __dmul_rn(v, v))), G);
-}
-
-// The (position, speed) lanes of rk4_step (integrator.hpp:39-68) for given
-// clamped stage brake values b1..b4.  k_i.d_position = stage speed, so the
-// position stages (dead code in the reference) are not formed.
-__device__ __forceinline__ void rk4_xv(double& x, double& v, double b1, double b2, double b3,
-                                       double b4, double D, double G, double dt, double half,
-                                       double sixth) {
-    const double k1 = accel(b1, v, D, G);
-    const double s2 = __dadd_rn(v, __dmul_rn(half, k1));
-    const double k2 = accel(b2, s2, D, G);
-    const double s3 = __dadd_rn(v, __dmul_rn(half, k2));
-    const double k3 = accel(b3, s3, D, G);
-    const double s4 = __dadd_rn(v, __dmul_rn(dt, k3));
-    const double k4 = accel(b4, s4, D, G);
-    // ((k1 + 2k2) + 2k3) + k4 with exact doubling folded into FMAs
-    const double cv = __dadd_rn(__fma_rn(2.0, k3, __fma_rn(2.0, k2, k1)), k4);
-    const double cx = __dadd_rn(__fma_rn(2.0, s3, __fma_rn(2.0, s2, v)), s4);
-    x = __dadd_rn(x, __dmul_rn(sixth, cx));
-    v = __dadd_rn(v, __dmul_rn(sixth, cv));
-}
 
 // Actuator lane of rk4_step for the no-table fallback (dynamics.hpp:130).
 __device__ __forceinline__ StageA actuator_stages(double a, double cmd, double inv_tau,
@@ -88,13 +59,6 @@ __device__ __forceinline__ StageA load_stage(const StageA* tab, int n) {
         return StageA{lo.x, lo.y, hi.x, hi.y};
     }
 }
-
-// v <= 0.0 (integrator.cpp:22) on the integer pipe: a binary64 pattern read
-// as int64 is <= 0 exactly for +0, -0 and every negative value, so the test
-// agrees with the FP compare for every non-NaN v and leaves the FP64 pipe to
-// the RK4 arithmetic.  (Only a sign-bit-set NaN would differ; finite inputs
-// cannot produce one.)
-__device__ __forceinline__ bool not_positive(double v) { return __double_as_longlong(v) <= 0ll; }
 
 template <int MODE>
 __device__ __forceinline__ double stage_value(const StageA* tab, int n, int s) {
