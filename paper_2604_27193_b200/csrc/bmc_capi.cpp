@@ -19,7 +19,18 @@ namespace bmc {
 namespace {
 
 constexpr size_t kTableCap = size_t{1} << 20;          // 32 MB of stage values
-constexpr uint64_t kDefaultChunk = uint64_t{1} << 22;  // 4M samples per pipeline slot
+// Pipeline chunk (samples per slot).  Every chunk's rollout costs at least
+// the latency of its longest sample (~1.2 ms for the default model) plus
+// its launches, while one chunk alone cannot overlap its host staging, H2D,
+// D2H and unpack with compute.  Measured on the B200 (tools/chunk_sweep.py,
+// profiles/round1_chunk_sweep.txt, and the 1e8 bench): up to 512k samples
+// one chunk, up to 2M two chunks, then four chunks capped at 4M samples.
+uint64_t default_chunk(uint64_t n) {
+    constexpr uint64_t kOne = uint64_t{1} << 19, kTwo = uint64_t{1} << 21, kMax = uint64_t{1} << 22;
+    if (n <= kOne) return n;
+    if (n <= kTwo) return (n + 1) / 2;
+    return std::min(kMax, (n + 3) / 4);
+}
 constexpr int kMaxCoarseSteps = 2048;
 constexpr int kBucketsTarget = 2000;  // step buckets; x2 clamp classes <= 4096 keys
 constexpr int kDefaultIlp = 1;
@@ -293,7 +304,7 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
                  bmc_result* host_out, const bmc_outputs* dev_out, bmc_run_info* info,
                  uint64_t* clamp_count) {
     using Clock = std::chrono::steady_clock;
-    const uint64_t chunk = std::min<uint64_t>(o.chunk_samples ? o.chunk_samples : kDefaultChunk, n);
+    const uint64_t chunk = std::min<uint64_t>(o.chunk_samples ? o.chunk_samples : default_chunk(n), n);
     const unsigned threads = resolve_threads(o.host_threads);
     Plan plan;
     int rc = make_plan(ctx, d, o, chunk, &plan);
