@@ -51,6 +51,7 @@ struct CudaExecOptions {
     int table_mode = 0;           ///< 0 auto (timing only)
     int ilp = 0;                  ///< samples per thread, 0 default (timing only)
     int sampler = 0;              ///< model-driven runs: 0 auto, 1 host pool, 2 device (timing only)
+    int test_block = 0;           ///< termination test every step (1) or per 8-step block (8) (timing only)
 };
 
 static_assert(sizeof(ScenarioSample) == sizeof(bmc_sample), "ScenarioSample layout");
@@ -98,6 +99,7 @@ inline bmc_run_opts opts_of(const CudaExecOptions& o) {
     r.chunk_samples = o.chunk_samples;
     r.ilp = o.ilp;
     r.sampler = o.sampler;
+    r.test_block = o.test_block;
     return r;
 }
 

@@ -107,6 +107,8 @@ typedef struct {
     int32_t ilp;            /* samples per thread: 0 = default, 1, or 2 (table modes) */
     int32_t sampler;        /* model-driven runs: 0 = auto (device when bmc_device_sampler_available),
                                1 = host pool, 2 = device (BMC_E_CONFIG when unavailable) */
+    int32_t test_block;     /* steps per termination-test block (ilp 1, table modes):
+                               0 = default, 1 = every step, 8 = blocked test + exact replay */
 } bmc_run_opts;
 
 /* Timing breakdown of one bmc_cuda_run call (seconds). */

@@ -81,7 +81,7 @@ class Outputs(C.Structure):
 class RunOpts(C.Structure):
     _fields_ = [("schedule", C.c_int32), ("block_threads", C.c_int32), ("table_mode", C.c_int32),
                 ("host_threads", C.c_int32), ("chunk_samples", C.c_uint64), ("ilp", C.c_int32),
-                ("sampler", C.c_int32)]
+                ("sampler", C.c_int32), ("test_block", C.c_int32)]
 
 
 class RunInfo(C.Structure):

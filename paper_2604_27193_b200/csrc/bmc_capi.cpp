@@ -35,6 +35,7 @@ constexpr int kMaxCoarseSteps = 2048;
 constexpr int kBucketsTarget = 2000;  // step buckets; x2 clamp classes <= 4096 keys
 constexpr int kDefaultIlp = 1;
 constexpr int kDefaultIlp2Block = 640;
+constexpr int kDefaultTestBlock = 8;  // profiles/round1_sweep_testblock.txt
 
 bool same_key(const WorldDerived& a, const WorldDerived& b) {
     return std::memcmp(&a, &b, sizeof a) == 0;
@@ -123,6 +124,9 @@ int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uin
     int ilp = opts.ilp == 0 ? kDefaultIlp : opts.ilp;
     if (ilp != 1 && ilp != 2) return fail(ctx, BMC_E_CONFIG, "execution.ilp: must be 1 or 2");
     if (mode == kTableNone) ilp = 1;
+    int tb = opts.test_block == 0 ? kDefaultTestBlock : opts.test_block;
+    if (tb != 1 && tb != 8) return fail(ctx, BMC_E_CONFIG, "execution.test_block: must be 1 or 8");
+    if (ilp != 1 || mode == kTableNone) tb = 1;
     int bt = opts.block_threads;
     if (bt == 0) bt = ilp == 2 ? kDefaultIlp2Block : (mode == kTableGlobal ? 256 : 1024);
     const bool ok_bt = ilp == 2 ? (bt == 512 || bt == 640 || bt == 768)
@@ -137,6 +141,7 @@ int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uin
     p.sched = sched;
     p.bt = bt;
     p.ilp = ilp;
+    p.test_block = tb;
     p.table = ctx->d_table.as<StageA>();
     p.table_len = ctx->t_len;
     p.table_min = ctx->t_min;
@@ -230,7 +235,7 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
     ra.counters = reinterpret_cast<unsigned long long*>(sc.counter.as<char>() + 8);
     if (ev) BMC_CK(ctx, cudaEventRecord(ev->r0, s));
     if (n > 0) {
-        BMC_CK(ctx, launch_rollout(ra, plan.mode, plan.bt, plan.ilp, s));
+        BMC_CK(ctx, launch_rollout(ra, plan.mode, plan.bt, plan.ilp, plan.test_block, s));
         ++nl;
     }
     if (ev) BMC_CK(ctx, cudaEventRecord(ev->r1, s));

@@ -97,6 +97,7 @@ struct Plan {
     int sched = kScheduleIndex;
     int bt = 1024;
     int ilp = 1;
+    int test_block = 1;
     const StageA* table = nullptr;
     int table_len = 0;
     double table_min = 0.0;

@@ -193,7 +193,91 @@ __device__ __forceinline__ LaneOut steps_from(const RolloutArgs& A, const StageA
     return LaneOut{c.x, M, false};
 }
 
+// Blocked termination test (UNR = kTestBlock): the V1 and V3 loops run
+// kTestBlock steps with no branch, folding hi_word(v) into a running
+// minimum; a lane whose minimum says it may have stopped replays the block
+// from its saved start state with the exact per-step test, so it returns
+// exactly the step and position simulate_rollout returns (integrator.cpp:
+// 20-26).  A false alarm (a positive subnormal v) replays to the identical
+// state and carries on.  Removing the per-step branch takes ~25 cycles off
+// each step's dependent chain (latency-bound small batches) and issue slots
+// off the FP64 pipe (tools/rk4_step_probe.cu).
+constexpr int kTestBlock = 8;
+
 template <int MODE>
+__device__ __forceinline__ LaneOut steps_from_blocked(const RolloutArgs& A, const StageA* tab,
+                                                      int len, Chain& c, int32_t n, int p1,
+                                                      int p2) {
+    const int32_t M = A.max_steps;
+    if (n < p2) {
+        StageA nx = load_stage<MODE>(tab, n);  // row n; rows n+1.. fetched one step ahead
+        for (; n + kTestBlock <= p1; n += kTestBlock) {
+            const double x0 = c.x, v0 = c.v;
+            int m = INT_MAX;
+#pragma unroll
+            for (int k = 0; k < kTestBlock; ++k) {
+                const StageA s = nx;
+                nx = load_stage<MODE>(tab, n + k + 1);  // n + k + 1 <= p1 <= head <= len - 1
+                rk4_xv(c.x, c.v, s.a0, s.a1, s.a2, s.a3, c.D, c.G, A.dt, A.half, A.sixth);
+                m = min(m, hi_word(c.v));
+            }
+            if (m <= 0) {
+                c.x = x0;
+                c.v = v0;
+#pragma unroll 1
+                for (int k = 0; k < kTestBlock; ++k) {
+                    const StageA s = load_stage<MODE>(tab, n + k);
+                    rk4_xv(c.x, c.v, s.a0, s.a1, s.a2, s.a3, c.D, c.G, A.dt, A.half, A.sixth);
+                    if (not_positive(c.v)) return LaneOut{c.x, n + k + 1, true};
+                }
+            }
+        }
+        for (; n < p1; ++n) {
+            const StageA s = nx;
+            nx = load_stage<MODE>(tab, n + 1);
+            rk4_xv(c.x, c.v, s.a0, s.a1, s.a2, s.a3, c.D, c.G, A.dt, A.half, A.sixth);
+            if (not_positive(c.v)) return LaneOut{c.x, n + 1, true};
+        }
+        for (; n < p2; ++n) {
+            const StageA s = nx;
+            nx = load_stage<MODE>(tab, n + 1);
+            rk4_xv(c.x, c.v, n < c.c0 ? s.a0 : c.F, n < c.c1 ? s.a1 : c.F,
+                   n < c.c2 ? s.a2 : c.F, n < c.c3 ? s.a3 : c.F, c.D, c.G, A.dt, A.half,
+                   A.sixth);
+            if (not_positive(c.v)) return LaneOut{c.x, n + 1, true};
+        }
+    }
+    if (n < M) {
+        const StageA s = load_stage<MODE>(tab, len - 1);
+        const double b0 = c.c0 <= n ? c.F : s.a0, b1 = c.c1 <= n ? c.F : s.a1;
+        const double b2 = c.c2 <= n ? c.F : s.a2, b3 = c.c3 <= n ? c.F : s.a3;
+        for (; n + kTestBlock <= M; n += kTestBlock) {
+            const double x0 = c.x, v0 = c.v;
+            int m = INT_MAX;
+#pragma unroll
+            for (int k = 0; k < kTestBlock; ++k) {
+                rk4_xv(c.x, c.v, b0, b1, b2, b3, c.D, c.G, A.dt, A.half, A.sixth);
+                m = min(m, hi_word(c.v));
+            }
+            if (m <= 0) {
+                c.x = x0;
+                c.v = v0;
+#pragma unroll 1
+                for (int k = 0; k < kTestBlock; ++k) {
+                    rk4_xv(c.x, c.v, b0, b1, b2, b3, c.D, c.G, A.dt, A.half, A.sixth);
+                    if (not_positive(c.v)) return LaneOut{c.x, n + k + 1, true};
+                }
+            }
+        }
+        for (; n < M; ++n) {
+            rk4_xv(c.x, c.v, b0, b1, b2, b3, c.D, c.G, A.dt, A.half, A.sixth);
+            if (not_positive(c.v)) return LaneOut{c.x, n + 1, true};
+        }
+    }
+    return LaneOut{c.x, M, false};
+}
+
+template <int MODE, int UNR>
 __device__ __forceinline__ LaneOut run_table(const RolloutArgs& A, const StageA* tab, int len,
                                              uint64_t j, unsigned mask) {
     Chain c;
@@ -201,6 +285,7 @@ __device__ __forceinline__ LaneOut run_table(const RolloutArgs& A, const StageA*
     const int head = min(len - 1, A.max_steps);
     const int p1 = min(__reduce_min_sync(mask, chain_cmin(c)), head);
     const int p2 = min(__reduce_max_sync(mask, chain_cmax(c)), head);
+    if (UNR == kTestBlock) return steps_from_blocked<MODE>(A, tab, len, c, 0, p1, p2);
     return steps_from<MODE>(A, tab, len, c, 0, p1, p2);
 }
 
@@ -310,7 +395,7 @@ __device__ __forceinline__ LaneOut run_inline(const RolloutArgs& A, uint64_t j) 
     return LaneOut{x, M, false};
 }
 
-template <int MODE, int BT, int ILP>
+template <int MODE, int BT, int ILP, int UNR>
 __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const StageA* tab = A.table;
@@ -356,7 +441,7 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
         const unsigned mask = __ballot_sync(0xffffffffu, i < A.n);
         if (i < A.n) {
             const uint64_t j = A.perm ? static_cast<uint64_t>(A.perm[i]) : i;
-            const LaneOut r = MODE == kTableNone ? run_inline(A, j) : run_table<MODE>(A, tab, len, j, mask);
+            const LaneOut r = MODE == kTableNone ? run_inline(A, j) : run_table<MODE, UNR>(A, tab, len, j, mask);
             store_out(A, j, r);
             const unsigned st = static_cast<unsigned>(max(r.steps, 0));
             my_steps += st;
@@ -537,12 +622,12 @@ __global__ void __launch_bounds__(512) fp64_probe_kernel(double* out, int iters,
     if (s == 12345.678) out[0] = s;  // never true; keeps the chains alive
 }
 
-template <int MODE, int BT, int ILP>
+template <int MODE, int BT, int ILP, int UNR = 1>
 cudaError_t launch_rollout_t(const RolloutArgs& a, cudaStream_t s) {
     size_t smem = 0;
     if (MODE == kTableShared) {
         smem = static_cast<size_t>(a.table_len) * sizeof(StageA);
-        const cudaError_t e = cudaFuncSetAttribute(rollout_kernel<MODE, BT, ILP>,
+        const cudaError_t e = cudaFuncSetAttribute(rollout_kernel<MODE, BT, ILP, UNR>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    static_cast<int>(smem));
         if (e != cudaSuccess) return e;
@@ -550,7 +635,7 @@ cudaError_t launch_rollout_t(const RolloutArgs& a, cudaStream_t s) {
     int dev = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, rollout_kernel<MODE, BT, ILP>, BT, smem);
+        &per_sm, rollout_kernel<MODE, BT, ILP, UNR>, BT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     // Persistent grid.  Small batches (the real-time case) spread their
@@ -566,12 +651,22 @@ cudaError_t launch_rollout_t(const RolloutArgs& a, cudaStream_t s) {
     }
     const uint64_t need = (groups + warps_per_block - 1) / warps_per_block;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(need, resident)));
-    rollout_kernel<MODE, BT, ILP><<<grid, static_cast<int>(warps_per_block * 32), smem, s>>>(a);
+    rollout_kernel<MODE, BT, ILP, UNR><<<grid, static_cast<int>(warps_per_block * 32), smem, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int MODE>
-cudaError_t launch_rollout_m(const RolloutArgs& a, int block_threads, int ilp, cudaStream_t s) {
+cudaError_t launch_rollout_m(const RolloutArgs& a, int block_threads, int ilp, int unroll,
+                             cudaStream_t s) {
+    if (unroll == kTestBlock && ilp == 1 && MODE != kTableNone) {
+        switch (block_threads) {
+            case 256: return launch_rollout_t<MODE, 256, 1, kTestBlock>(a, s);
+            case 512: return launch_rollout_t<MODE, 512, 1, kTestBlock>(a, s);
+            case 768: return launch_rollout_t<MODE, 768, 1, kTestBlock>(a, s);
+            case 1024: return launch_rollout_t<MODE, 1024, 1, kTestBlock>(a, s);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     if (ilp == 2 && MODE != kTableNone) {
         switch (block_threads) {
             case 512: return launch_rollout_t<MODE, 512, 2>(a, s);
@@ -607,11 +702,11 @@ int sm_count(int device) {
 }
 
 cudaError_t launch_rollout(const RolloutArgs& a, int table_mode, int block_threads, int ilp,
-                           cudaStream_t s) {
+                           int unroll, cudaStream_t s) {
     switch (table_mode) {
-        case kTableShared: return launch_rollout_m<kTableShared>(a, block_threads, ilp, s);
-        case kTableGlobal: return launch_rollout_m<kTableGlobal>(a, block_threads, ilp, s);
-        case kTableNone: return launch_rollout_m<kTableNone>(a, block_threads, 1, s);
+        case kTableShared: return launch_rollout_m<kTableShared>(a, block_threads, ilp, unroll, s);
+        case kTableGlobal: return launch_rollout_m<kTableGlobal>(a, block_threads, ilp, unroll, s);
+        case kTableNone: return launch_rollout_m<kTableNone>(a, block_threads, 1, 1, s);
         default: return cudaErrorInvalidValue;
     }
 }

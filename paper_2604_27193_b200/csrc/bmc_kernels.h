@@ -103,7 +103,7 @@ int sm_count(int device);
 
 // Persistent launch: grid = min(resident CTAs, 32-sample groups / warps per CTA).
 cudaError_t launch_rollout(const RolloutArgs& a, int table_mode, int block_threads, int ilp,
-                           cudaStream_t s);
+                           int unroll, cudaStream_t s);
 cudaError_t launch_predict(const PredictArgs& a, cudaStream_t s);
 cudaError_t launch_fp64_probe(double* out, int iters, uint64_t* ops, cudaStream_t s);
 cudaError_t launch_bin_scan(unsigned int* hist_to_cursor, int buckets, cudaStream_t s);

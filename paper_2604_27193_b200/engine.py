@@ -188,9 +188,9 @@ class CudaExecutor:
 
     @staticmethod
     def _opts(schedule="default", block_threads=0, table="auto", host_threads=0, chunk=0, ilp=0,
-              sampler="auto"):
+              sampler="auto", test_block=0):
         return N.RunOpts(SCHEDULE[schedule], block_threads, TABLE[table], host_threads, chunk,
-                         ilp, SAMPLER[sampler])
+                         ilp, SAMPLER[sampler], test_block)
 
     # -------------------------------------------------------------- executor
     def run(self, samples: np.ndarray, world: SimWorld = SimWorld(), out: np.ndarray = None,

@@ -64,16 +64,18 @@ def test_scheduling_knobs_never_change_bits(ref, executor, schedule, table, bloc
     assert_parity(ref, want, rep.results)
 
 
-@pytest.mark.parametrize("ilp,block", [(1, 1024), (1, 768), (2, 640), (2, 512)])
+@pytest.mark.parametrize("ilp,block,tb", [(1, 1024, 1), (1, 768, 1), (2, 640, 1), (2, 512, 1),
+                                          (1, 1024, 8), (1, 512, 8)])
 @pytest.mark.parametrize("table", ["shared", "global"])
 @pytest.mark.parametrize("w", [World(), World(t_max=3.0), World(actuator_tau=30.0),
                                World(t_max=0.0005), World(t_max=0.003)],
                          ids=["default", "tmax3", "tau30", "one_step", "three_steps"])
-def test_loop_variants_never_change_bits(ref, executor, ilp, block, table, w):
+def test_loop_variants_never_change_bits(ref, executor, ilp, block, tb, table, w):
     # odd/even step counts, stops inside each warp-uniform phase, horizons
     samples, _ = ref.draw_batch(Model.mixed(29), 5000)
     want, _, _ = ref.run(samples, w, "parallel")
-    rep = executor.run(samples, to_world(w), table=table, block_threads=block, ilp=ilp)
+    rep = executor.run(samples, to_world(w), table=table, block_threads=block, ilp=ilp,
+                       test_block=tb)
     assert_parity(ref, want, rep.results)
 
 

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--occupancy", action="store_true")
+    ap.add_argument("--testblock", action="store_true", help="per-step vs blocked termination test")
     a = ap.parse_args()
     n = int(a.samples)
     model = bmc.UncertaintyModel.mixed(3) if a.model == "mixed" else bmc.UncertaintyModel(seed=3)
@@ -45,22 +46,24 @@ def main():
             ex.sync()
         print("profile run done", ex.last_kernel_ms())
         return
-    configs = [(s, t, b, 1) for s, t, b in itertools.product(
+    configs = [(s, t, b, 1, 1) for s, t, b in itertools.product(
         ["binned", "index"], ["shared", "global", "none"], [256, 512, 768, 1024])]
-    configs += [(s, t, b, 2) for s, t, b in itertools.product(
+    configs += [(s, t, b, 2, 1) for s, t, b in itertools.product(
         ["binned"], ["shared", "global"], [512, 640, 768])]
     if a.quick:
         configs = [c for c in configs if c[0] == "binned" and c[2] >= 512 and c[1] != "none"]
     if a.occupancy:
-        configs = [("binned", t, b, 1) for t in ("shared", "global") for b in (384, 640, 1024)]
-    for sched, table, bt, ilp in configs:
+        configs = [("binned", t, b, 1, 1) for t in ("shared", "global") for b in (384, 640, 1024)]
+    if a.testblock:
+        configs = [("binned", "shared", b, 1, tb) for tb in (1, 8) for b in (768, 1024)]
+    for sched, table, bt, ilp, tb in configs:
         if table == "none" and sched == "binned":
             continue
         best = None
         for _ in range(a.reps):
             tot.zero_()
             ex.rollout_device(dev, (d, st, hz), total_steps=tot, schedule=sched, table=table,
-                              block_threads=bt, ilp=ilp)
+                              block_threads=bt, ilp=ilp, test_block=tb)
             ex.sync()
             r, p = ex.last_kernel_ms()
             if best is None or r + p < best[0] + best[1]:
@@ -68,7 +71,7 @@ def main():
         steps = int(tot.item())
         r, p = best
         _, _, eff = ex.lane_efficiency()
-        print(f"{a.model:7s} n={n} sched={sched:6s} table={table:6s} bt={bt:4d} ilp={ilp} "
+        print(f"{a.model:7s} n={n} sched={sched:6s} table={table:6s} bt={bt:4d} ilp={ilp} tb={tb} "
               f"rollout {r:9.3f} ms  predict {p:7.3f} ms  steps/s {steps/(r*1e-3):.4e}  "
               f"exec-op/s {32*steps/(r*1e-3)/1e12:.3f} T ({32*steps/(r*1e-3)/peak:.3f} of probe)"
               f"  algo {57*steps/(r*1e-3)/peak:.3f}  lane-eff {eff:.4f}", flush=True)

@@ -262,8 +262,8 @@ int main() {
     cudaMemcpy(gtab, h, sizeof h, cudaMemcpyHostToDevice);
     cudaMemcpyToSymbol(c_tab, h, kConstRows * sizeof(StageA));
     printf("executed FP64 op rate of the 32-op RK4 step (T op/s); -1 = does not fit\n");
-    printf("%-18s %8s %8s %8s %8s %8s %8s\n", "variant", "w16", "w24", "w32", "w48", "w64", "");
-    const int ws[] = {16, 24, 32, 48, 64};
+    printf("%-18s %8s %8s %8s %8s %8s %8s %8s\n", "variant", "w1", "w4", "w16", "w24", "w32", "w48", "w64");
+    const int ws[] = {1, 4, 16, 24, 32, 48, 64};
 #define ROW(M, C, name)                                                         \
     {                                                                           \
         printf("%-18s", name);                                                  \
@@ -287,6 +287,7 @@ int main() {
     ROW(34, 1, "ctable+vote4 C=1");
     ROW(38, 1, "ctable+vote8 C=1");
     ROW(34, 2, "ctable+vote4 C=2");
+    printf("cycles per step for one warp per SM (latency-bound regime): rate -> 148*32*32 ops per step\n");
     printf("%-18s", "ptable+vote8 C=1");
     for (int w : ws) printf(" %8.3f", run_param<8>(w, sms, out) / 1e12);
     printf("\n");
