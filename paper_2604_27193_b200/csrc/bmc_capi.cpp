@@ -33,7 +33,11 @@ uint64_t default_chunk(uint64_t n) {
 }
 constexpr int kMaxCoarseSteps = 2048;
 constexpr int kBucketsTarget = 2000;  // step buckets; x2 clamp classes <= 4096 keys
-constexpr int kDefaultIlp = 1;
+// Two chains per thread (one table-row load feeds both) once a launch has
+// enough 64-sample groups to fill the GPU several times; below that the
+// latency of each thread's doubled work dominates (tools/kernel_sweep.py
+// --ilpcmp, profiles/round1_sweep_ilp.txt: crossover ~1M samples).
+constexpr uint64_t kIlp2MinSamples = uint64_t{1} << 20;
 constexpr int kDefaultIlp2Block = 640;
 constexpr int kDefaultTestBlock = 8;  // profiles/round1_sweep_testblock.txt
 
@@ -109,7 +113,6 @@ int ensure_table(bmc_ctx* ctx, const WorldDerived& d) {
 
 int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uint64_t n,
               Plan* plan) {
-    (void)n;
     const int rc = ensure_table(ctx, d);
     if (rc != BMC_OK) return rc;
     Plan p;
@@ -121,12 +124,12 @@ int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uin
     int sched = opts.schedule;
     if (sched == kScheduleDefault) sched = kScheduleBinned;
     if (ctx->coarse_len == 0 || mode == kTableNone) sched = kScheduleIndex;
-    int ilp = opts.ilp == 0 ? kDefaultIlp : opts.ilp;
+    int ilp = opts.ilp != 0 ? opts.ilp : (n >= kIlp2MinSamples ? 2 : 1);
     if (ilp != 1 && ilp != 2) return fail(ctx, BMC_E_CONFIG, "execution.ilp: must be 1 or 2");
     if (mode == kTableNone) ilp = 1;
     int tb = opts.test_block == 0 ? kDefaultTestBlock : opts.test_block;
     if (tb != 1 && tb != 8) return fail(ctx, BMC_E_CONFIG, "execution.test_block: must be 1 or 8");
-    if (ilp != 1 || mode == kTableNone) tb = 1;
+    if (mode == kTableNone) tb = 1;
     int bt = opts.block_threads;
     if (bt == 0) bt = ilp == 2 ? kDefaultIlp2Block : (mode == kTableGlobal ? 256 : 1024);
     const bool ok_bt = ilp == 2 ? (bt == 512 || bt == 640 || bt == 768)

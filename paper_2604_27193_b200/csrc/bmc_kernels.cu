@@ -295,8 +295,10 @@ __device__ __forceinline__ LaneOut run_table(const RolloutArgs& A, const StageA*
 // first one stops (one combined termination test per step, no per-chain
 // latching in the hot loop); the survivor then finishes on the single-chain
 // loop from that step.  Shared per-thread state (table row, loop control)
-// is amortised over two dependency chains.
-template <int MODE>
+// is amortised over two dependency chains: one table-row load feeds both.
+// BLK: the V1 and V3 loops use the blocked termination test of
+// steps_from_blocked (running minimum over both chains, exact replay).
+template <int MODE, bool BLK>
 __device__ __forceinline__ void run_table2(const RolloutArgs& A, const StageA* tab, int len,
                                            uint64_t j0, uint64_t j1, bool ok0, bool ok1,
                                            LaneOut& r0, LaneOut& r1) {
@@ -313,7 +315,39 @@ __device__ __forceinline__ void run_table2(const RolloutArgs& A, const StageA* t
     bool hit = false;
     if (n < p2) {
         StageA nx = load_stage<MODE>(tab, 0);
-        for (; n < p1; ++n) {
+        if (BLK) {
+            for (; n + kTestBlock <= p1; n += kTestBlock) {
+                const double xa0 = a.x, va0 = a.v, xb0 = b.x, vb0 = b.v;
+                int m = INT_MAX;
+#pragma unroll
+                for (int k = 0; k < kTestBlock; ++k) {
+                    const StageA s = nx;
+                    nx = load_stage<MODE>(tab, n + k + 1);  // n + k + 1 <= p1 <= head
+                    rk4_xv(a.x, a.v, s.a0, s.a1, s.a2, s.a3, a.D, a.G, A.dt, A.half, A.sixth);
+                    rk4_xv(b.x, b.v, s.a0, s.a1, s.a2, s.a3, b.D, b.G, A.dt, A.half, A.sixth);
+                    m = min(m, min(hi_word(a.v), hi_word(b.v)));
+                }
+                if (m <= 0) {
+                    a.x = xa0;
+                    a.v = va0;
+                    b.x = xb0;
+                    b.v = vb0;
+#pragma unroll 1
+                    for (int k = 0; k < kTestBlock; ++k) {
+                        const StageA s = load_stage<MODE>(tab, n + k);
+                        rk4_xv(a.x, a.v, s.a0, s.a1, s.a2, s.a3, a.D, a.G, A.dt, A.half, A.sixth);
+                        rk4_xv(b.x, b.v, s.a0, s.a1, s.a2, s.a3, b.D, b.G, A.dt, A.half, A.sixth);
+                        if (not_positive(a.v) | not_positive(b.v)) {
+                            n += k;
+                            hit = true;
+                            break;
+                        }
+                    }
+                    if (hit) break;
+                }
+            }
+        }
+        for (; !hit && n < p1; ++n) {
             const StageA s = nx;
             nx = load_stage<MODE>(tab, n + 1);
             rk4_xv(a.x, a.v, s.a0, s.a1, s.a2, s.a3, a.D, a.G, A.dt, A.half, A.sixth);
@@ -346,7 +380,36 @@ __device__ __forceinline__ void run_table2(const RolloutArgs& A, const StageA* t
         const double a2 = a.c2 <= n ? a.F : s.a2, a3 = a.c3 <= n ? a.F : s.a3;
         const double b0 = b.c0 <= n ? b.F : s.a0, b1 = b.c1 <= n ? b.F : s.a1;
         const double b2 = b.c2 <= n ? b.F : s.a2, b3 = b.c3 <= n ? b.F : s.a3;
-        for (; n < M; ++n) {
+        if (BLK) {
+            for (; n + kTestBlock <= M; n += kTestBlock) {
+                const double xa0 = a.x, va0 = a.v, xb0 = b.x, vb0 = b.v;
+                int m = INT_MAX;
+#pragma unroll
+                for (int k = 0; k < kTestBlock; ++k) {
+                    rk4_xv(a.x, a.v, a0, a1, a2, a3, a.D, a.G, A.dt, A.half, A.sixth);
+                    rk4_xv(b.x, b.v, b0, b1, b2, b3, b.D, b.G, A.dt, A.half, A.sixth);
+                    m = min(m, min(hi_word(a.v), hi_word(b.v)));
+                }
+                if (m <= 0) {
+                    a.x = xa0;
+                    a.v = va0;
+                    b.x = xb0;
+                    b.v = vb0;
+#pragma unroll 1
+                    for (int k = 0; k < kTestBlock; ++k) {
+                        rk4_xv(a.x, a.v, a0, a1, a2, a3, a.D, a.G, A.dt, A.half, A.sixth);
+                        rk4_xv(b.x, b.v, b0, b1, b2, b3, b.D, b.G, A.dt, A.half, A.sixth);
+                        if (not_positive(a.v) | not_positive(b.v)) {
+                            n += k;
+                            hit = true;
+                            break;
+                        }
+                    }
+                    if (hit) break;
+                }
+            }
+        }
+        for (; !hit && n < M; ++n) {
             rk4_xv(a.x, a.v, a0, a1, a2, a3, a.D, a.G, A.dt, A.half, A.sixth);
             rk4_xv(b.x, b.v, b0, b1, b2, b3, b.D, b.G, A.dt, A.half, A.sixth);
             if (not_positive(a.v) | not_positive(b.v)) {
@@ -366,7 +429,8 @@ __device__ __forceinline__ void run_table2(const RolloutArgs& A, const StageA* t
     if (sa && sb) return;
     // finish the survivor from step n + 1 on the single-chain loop
     Chain& c = sa ? b : a;
-    const LaneOut r = steps_from<MODE>(A, tab, len, c, n + 1, p1, p2);
+    const LaneOut r = BLK ? steps_from_blocked<MODE>(A, tab, len, c, n + 1, p1, p2)
+                          : steps_from<MODE>(A, tab, len, c, n + 1, p1, p2);
     if (sa) {
         r1 = r;
     } else {
@@ -421,7 +485,7 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
             const uint64_t j0 = ok0 ? (A.perm ? static_cast<uint64_t>(A.perm[i0]) : i0) : 0;
             const uint64_t j1 = ok1 ? (A.perm ? static_cast<uint64_t>(A.perm[i1]) : i1) : 0;
             LaneOut r0, r1;
-            run_table2<MODE>(A, tab, len, j0, j1, ok0, ok1, r0, r1);
+            run_table2<MODE, UNR == kTestBlock>(A, tab, len, j0, j1, ok0, ok1, r0, r1);
             if (ok0) {
                 store_out(A, j0, r0);
                 my_steps += static_cast<unsigned>(max(r0.steps, 0));
@@ -658,6 +722,14 @@ cudaError_t launch_rollout_t(const RolloutArgs& a, cudaStream_t s) {
 template <int MODE>
 cudaError_t launch_rollout_m(const RolloutArgs& a, int block_threads, int ilp, int unroll,
                              cudaStream_t s) {
+    if (unroll == kTestBlock && ilp == 2 && MODE != kTableNone) {
+        switch (block_threads) {
+            case 512: return launch_rollout_t<MODE, 512, 2, kTestBlock>(a, s);
+            case 640: return launch_rollout_t<MODE, 640, 2, kTestBlock>(a, s);
+            case 768: return launch_rollout_t<MODE, 768, 2, kTestBlock>(a, s);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     if (unroll == kTestBlock && ilp == 1 && MODE != kTableNone) {
         switch (block_threads) {
             case 256: return launch_rollout_t<MODE, 256, 1, kTestBlock>(a, s);

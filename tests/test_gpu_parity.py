@@ -65,7 +65,7 @@ def test_scheduling_knobs_never_change_bits(ref, executor, schedule, table, bloc
 
 
 @pytest.mark.parametrize("ilp,block,tb", [(1, 1024, 1), (1, 768, 1), (2, 640, 1), (2, 512, 1),
-                                          (1, 1024, 8), (1, 512, 8)])
+                                          (1, 1024, 8), (1, 512, 8), (2, 640, 8), (2, 768, 8)])
 @pytest.mark.parametrize("table", ["shared", "global"])
 @pytest.mark.parametrize("w", [World(), World(t_max=3.0), World(actuator_tau=30.0),
                                World(t_max=0.0005), World(t_max=0.003)],

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--occupancy", action="store_true")
     ap.add_argument("--testblock", action="store_true", help="per-step vs blocked termination test")
+    ap.add_argument("--ilpcmp", action="store_true", help="ilp 1 (1024) vs ilp 2 (640), blocked test")
     a = ap.parse_args()
     n = int(a.samples)
     model = bmc.UncertaintyModel.mixed(3) if a.model == "mixed" else bmc.UncertaintyModel(seed=3)
@@ -56,6 +57,9 @@ def main():
         configs = [("binned", t, b, 1, 1) for t in ("shared", "global") for b in (384, 640, 1024)]
     if a.testblock:
         configs = [("binned", "shared", b, 1, tb) for tb in (1, 8) for b in (768, 1024)]
+        configs += [("binned", "shared", b, 2, 8) for b in (512, 640, 768)]
+    if a.ilpcmp:
+        configs = [("binned", "shared", 1024, 1, 8), ("binned", "shared", 640, 2, 8)]
     for sched, table, bt, ilp, tb in configs:
         if table == "none" and sched == "binned":
             continue

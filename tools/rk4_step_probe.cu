@@ -301,6 +301,8 @@ int main() {
     ROW3(28, 1, "laneb+min8 C=1");
     ROW(0, 2, "pure C=2");
     ROW(2, 2, "table C=2");
+    ROW(18, 2, "table+min8 C=2");
+    ROW(14, 2, "table+min4 C=2");
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         printf("CUDA error: %s\n", cudaGetErrorString(e));
