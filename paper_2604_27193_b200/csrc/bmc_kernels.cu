@@ -733,7 +733,9 @@ cudaError_t launch_rollout_m(const RolloutArgs& a, int block_threads, int ilp, i
     if (unroll == kTestBlock && ilp == 1 && MODE != kTableNone) {
         switch (block_threads) {
             case 256: return launch_rollout_t<MODE, 256, 1, kTestBlock>(a, s);
+            case 384: return launch_rollout_t<MODE, 384, 1, kTestBlock>(a, s);
             case 512: return launch_rollout_t<MODE, 512, 1, kTestBlock>(a, s);
+            case 640: return launch_rollout_t<MODE, 640, 1, kTestBlock>(a, s);
             case 768: return launch_rollout_t<MODE, 768, 1, kTestBlock>(a, s);
             case 1024: return launch_rollout_t<MODE, 1024, 1, kTestBlock>(a, s);
             default: return cudaErrorInvalidValue;

@@ -45,6 +45,24 @@ def test_criterion1_matrix(ref, executor, seed, n):
     assert rep.total_steps == int(want["steps"].sum())
 
 
+def test_large_batch_default_plan(ref, executor):
+    # >= 2^20 samples per launch: the planner's two-chains-per-thread rollout
+    n = (1 << 20) + 12345
+    samples, _ = ref.draw_batch(Model.mixed(41), n)
+    want, _, _ = ref.run(samples, World(), "parallel")
+    import torch
+    terms = bmc.stage_terms(samples)
+    dev = [torch.from_numpy(terms[i]).cuda() for i in range(4)]
+    d = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = torch.empty(n, dtype=torch.int32, device="cuda")
+    hz = torch.empty(n, dtype=torch.uint8, device="cuda")
+    executor.rollout_device(dev, (d, st, hz))
+    executor.sync()
+    assert np.array_equal(d.cpu().numpy().view(np.uint64), want["stop_distance"].view(np.uint64))
+    assert np.array_equal(st.cpu().numpy(), want["steps"].astype(np.int32))
+    assert np.array_equal(hz.cpu().numpy(), want["hit_horizon"].astype(np.uint8))
+
+
 def test_mixed_model_with_horizons(ref, executor):
     samples, _ = ref.draw_batch(Model.mixed(3), 100000)
     want, _, _ = ref.run(samples, World(), "parallel")

@@ -68,3 +68,23 @@ def test_random_statistics(ref, executor, m, n, bw):
     for risk in (0.5, 0.1, 0.01):
         a, b = executor.min_safe_headway(d, hz, risk), ref.min_safe_headway(res, risk)
         assert a == b or (math.isinf(a) and math.isinf(b))
+
+
+# every rollout loop variant the planner can pick (chains per thread, block
+# size, termination-test block, table placement) on random worlds / models
+variants = st.sampled_from([
+    dict(ilp=1, block_threads=1024, test_block=8), dict(ilp=1, block_threads=256, test_block=1),
+    dict(ilp=2, block_threads=640, test_block=8), dict(ilp=2, block_threads=512, test_block=1),
+    dict(ilp=2, block_threads=768, test_block=8, table="global"),
+    dict(ilp=1, block_threads=384, test_block=8, table="global"),
+])
+
+
+@settings(max_examples=25, deadline=None, suppress_health_check=list(HealthCheck))
+@given(w=worlds, m=models, n=st.integers(1, 5000), opts=variants)
+def test_random_loop_variants_bit_exact(ref, executor, w, m, n, opts):
+    samples, _ = ref.draw_batch(m, n)
+    want, _, _ = ref.run(samples, w, "parallel")
+    sw = bmc.SimWorld(*w.as_array().tolist())
+    got = executor.run(samples, sw, **opts).results
+    assert results_bitwise_equal(want, got), opts
