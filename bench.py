@@ -39,6 +39,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ALGO_FLOPS_PER_STEP = 57   # reference formulation, per RK4 step
+# Algorithmic HBM bytes per sample of the streaming stages around the rollout:
+#   sample stream = predict (reads v0, floor, drag, grade: 32 B; writes a 2-B key)
+#                 + binning scatter (reads key + 32 B terms; writes the 32-B packed
+#                   record + 4-B slot index)
+#   result stream = unpermute (reads the 4-B slot + 16-B packed output; writes
+#                   stop_distance 8 B + steps 4 B + hit_horizon 1 B)
+SAMPLE_STREAM_BYTES = 32 + 2 + 2 + 32 + 32 + 4
+RESULT_STREAM_BYTES = 4 + 16 + 8 + 4 + 1
 EXEC_FLOPS_PER_STEP = 32   # this kernel (actuator table + exact-doubling FMA)
 SPEC_FP64_OPS = 148 * 64 * 1.965e9  # nominal DADD/DMUL rate at max clock
 
@@ -314,6 +322,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     headways = [t * model.initial_speed[0] for t in ttc]
     launches = [0]
     kernel_ms = []
+    stage_ms = []
 
     from paper_2604_27193_b200 import distributed as D
     cdev = coll_device or f"cuda:{local_rank}"
@@ -349,7 +358,9 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
         ex.rollout_device(dev_terms, (d, st, hz), sw, total_steps=total_steps)
         nl = ex.last_launches()
         if record:
-            kernel_ms.append(ex.last_kernel_ms()[0])
+            b_ms, r_ms, u_ms = ex.last_stage_ms()
+            kernel_ms.append(r_ms)
+            stage_ms.append((b_ms, u_ms))
         launches[1] = 0
         # statistics merged over all ranks (one allreduce per quantity)
         counts = D.exceedance_counts(shard, coll, headways)
@@ -395,6 +406,27 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
                           "algorithmic_bytes_per_sample": tj["algorithmic_bytes_per_sample"],
                           "source": tj["source"] + ", scaled to this launch's sample count"}
     steps_per_launch = steps_sum / args.steps
+    hbm_peak, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    ppath = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(ppath):
+        hbm_peak, hbm_src = float(json.load(open(ppath))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    bin_ms = sum(b for b, _ in stage_ms) / len(stage_ms)
+    unp_ms = sum(u for _, u in stage_ms) / len(stage_ms)
+
+    def stream(bytes_per_sample, ms, what):
+        gbs = bytes_per_sample * n / (ms * 1e-3) / 1e9 if ms > 0 else None
+        return {"what": what, "bytes_per_sample": bytes_per_sample, "ms": ms, "gb_per_s": gbs,
+                "frac_of_hbm_peak": gbs / hbm_peak if gbs else None}
+
+    hbm_streams = {
+        "peak_gb_per_s": hbm_peak, "peak_source": hbm_src,
+        "sample_stream": stream(SAMPLE_STREAM_BYTES, bin_ms,
+                                "predict + binning scatter: terms in, packed sorted records out"),
+        "rollout": stream(traffic / n if traffic else 48.0, roll_ms,
+                          "rollout kernel DRAM bytes (ncu) over its time -- FP64-bound"),
+        "result_stream": stream(RESULT_STREAM_BYTES, unp_ms,
+                                "unpermute: packed sorted outputs -> index-order outputs"),
+    }
     achieved = ALGO_FLOPS_PER_STEP * steps_per_launch / (roll_ms * 1e-3)
     executed = EXEC_FLOPS_PER_STEP * steps_per_launch / (roll_ms * 1e-3)
 
@@ -465,6 +497,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
                          "peak_source": "measured in-run: unfused DADD/DMUL probe "
                                         "(MEASURED_PEAKS.json has no FP64 entry)",
                          "spec_peak_tflops": SPEC_FP64_OPS / 1e12},
+            "hbm_streams": hbm_streams,
             "e2e": e2e,
             "device_sampler": dsamp,
             "latency_25k": latency,

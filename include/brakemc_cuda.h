@@ -219,6 +219,10 @@ int bmc_cuda_rollout_device(bmc_ctx* ctx, const bmc_terms* terms, size_t n,
 /* Last rollout kernel's device time in ms, via CUDA events recorded around
  * it on its own stream (waits for the closing event). */
 int bmc_cuda_last_kernel_ms(bmc_ctx* ctx, float* rollout_ms, float* predict_ms);
+/* Per-stage device time of the last device-resident rollout (ms, CUDA
+ * events on its stream): predictor + binning scatter, rollout kernel,
+ * unpermute (0 when a stage did not run).  Waits for the closing events. */
+int bmc_cuda_last_stage_ms(bmc_ctx* ctx, float* bin_ms, float* rollout_ms, float* unpermute_ms);
 /* Executed RK4 steps and lane slots (sum over 32-sample groups of
  * active lanes x longest lane) of the last rollout launch on the context's
  * stream; steps / slots is the SIMT lane efficiency.  Synchronises. */

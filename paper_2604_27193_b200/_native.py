@@ -142,6 +142,8 @@ SIGNATURES = [
     ("bmc_cuda_rollout_device", C.c_int, [_P, C.POINTER(Terms), C.c_size_t, C.POINTER(World),
                                           C.POINTER(RunOpts), C.POINTER(Outputs), _P, _P]),
     ("bmc_cuda_last_kernel_ms", C.c_int, [_P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    ("bmc_cuda_last_stage_ms", C.c_int, [_P, C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                         C.POINTER(C.c_float)]),
     ("bmc_cuda_last_launches", C.c_int, [_P, C.POINTER(C.c_uint32)]),
     ("bmc_cuda_last_lane_stats", C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("bmc_cuda_summarize", C.c_int, [_P, _P, _P, C.c_size_t, C.c_double, C.POINTER(Summary), _P,

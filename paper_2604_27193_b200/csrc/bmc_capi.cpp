@@ -23,10 +23,12 @@ constexpr size_t kTableCap = size_t{1} << 20;          // 32 MB of stage values
 // the latency of its longest sample (~1.2 ms for the default model) plus
 // its launches, while one chunk alone cannot overlap its host staging, H2D,
 // D2H and unpack with compute.  Measured on the B200 (tools/chunk_sweep.py,
-// profiles/round1_chunk_sweep.txt, and the 1e8 bench): up to 512k samples
-// one chunk, up to 2M two chunks, then four chunks capped at 4M samples.
+// profiles/round1_chunk_sweep.txt, and the 1e8 bench; each slot has its own
+// compute stream, so a chunk's binning and rollout fill the previous
+// chunk's tail): up to 128k samples one chunk, up to 8M two chunks, then
+// four chunks capped at 4M samples.
 uint64_t default_chunk(uint64_t n) {
-    constexpr uint64_t kOne = uint64_t{1} << 19, kTwo = uint64_t{1} << 21, kMax = uint64_t{1} << 22;
+    constexpr uint64_t kOne = uint64_t{1} << 17, kTwo = uint64_t{1} << 23, kMax = uint64_t{1} << 22;
     if (n <= kOne) return n;
     if (n <= kTwo) return (n + 1) / 2;
     return std::min(kMax, (n + 3) / 4);
@@ -242,10 +244,15 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
         ++nl;
     }
     if (ev) BMC_CK(ctx, cudaEventRecord(ev->r1, s));
+    if (ev) ev->unpermuted = false;
     if (packed && n > 0 && (out.stop_distance || out.steps || out.hit_horizon)) {
         BMC_CK(ctx, launch_unpermute(sc.packed_out.as<PackedOut>(), sc.perm.as<uint32_t>(), n,
                                      out.stop_distance, out.steps, out.hit_horizon, s));
         ++nl;
+        if (ev) {
+            BMC_CK(ctx, cudaEventRecord(ev->u1, s));
+            ev->unpermuted = true;
+        }
     }
     if (launches) *launches += nl;
     return BMC_OK;
@@ -334,8 +341,11 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
     }
     BMC_CK(ctx, ctx->total_steps.reserve(sizeof(unsigned long long)));
     BMC_CK(ctx, cudaMemsetAsync(ctx->total_steps.p, 0, sizeof(unsigned long long), ctx->stream));
-    rc = reserve_scratch(ctx, ctx->scratch, plan, chunk);
-    if (rc != BMC_OK) return rc;
+    for (auto& s : ctx->slots) {
+        if ((rc = reserve_scratch(ctx, s.sc, plan, chunk)) != BMC_OK) return rc;
+    }
+    // the slot streams start after the counters above are cleared
+    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
 
     double kernel_ms = 0.0, predict_ms = 0.0;
     uint32_t launches = 0;
@@ -393,7 +403,7 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
             da.grade = dt0 + 3 * s.len;
             da.clamps = ctx->draw_ctr.as<unsigned long long>();
             da.flags = reinterpret_cast<unsigned int*>(ctx->draw_ctr.as<char>() + 8);
-            BMC_CK(ctx, launch_draw_terms(da, ctx->sms, ctx->stream));
+            BMC_CK(ctx, launch_draw_terms(da, ctx->sms, s.compute));
             ++launches;
         } else {
             double* hv0 = s.h_terms.as<double>();
@@ -418,13 +428,13 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
                 },
                 threads);
             if (status != BMC_OK) {
-                cudaStreamSynchronize(ctx->stream);
+                for (auto& q : ctx->slots) cudaStreamSynchronize(q.compute);
                 cudaStreamSynchronize(ctx->d2h);
                 return fail(ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
             }
             BMC_CK(ctx, cudaMemcpyAsync(s.d_terms.p, s.h_terms.p, s.len * 32, cudaMemcpyHostToDevice, ctx->h2d));
             BMC_CK(ctx, cudaEventRecord(s.h2d_done, ctx->h2d));
-            BMC_CK(ctx, cudaStreamWaitEvent(ctx->stream, s.h2d_done, 0));
+            BMC_CK(ctx, cudaStreamWaitEvent(s.compute, s.h2d_done, 0));
         }
         const double* dv0 = s.d_terms.as<double>();
         const bmc_terms terms{dv0, dv0 + s.len, dv0 + 2 * s.len, dv0 + 3 * s.len};
@@ -439,11 +449,11 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
                                dev_out->steps ? dev_out->steps + s.offset : nullptr,
                                dev_out->hit_horizon ? dev_out->hit_horizon + s.offset : nullptr};
         }
-        rc = enqueue_rollout(ctx, plan, ctx->scratch, terms, s.len, outs,
-                             ctx->total_steps.as<unsigned long long>(), ctx->stream, &s.kev,
+        rc = enqueue_rollout(ctx, plan, s.sc, terms, s.len, outs,
+                             ctx->total_steps.as<unsigned long long>(), s.compute, &s.kev,
                              &launches);
         if (rc != BMC_OK) return rc;
-        BMC_CK(ctx, cudaEventRecord(s.compute_done, ctx->stream));
+        BMC_CK(ctx, cudaEventRecord(s.compute_done, s.compute));
         BMC_CK(ctx, cudaStreamWaitEvent(ctx->d2h, s.compute_done, 0));
         if (host_out) {
             // d_out holds d (8B), steps (4B), horizon (1B) blocks contiguously
@@ -525,7 +535,8 @@ int bmc_cuda_init(int device, bmc_ctx** out) {
         return fail(nullptr, BMC_E_CUDA, std::string("context setup: ") + cudaGetErrorString(e));
     }
     for (auto& s : ctx->slots) {
-        if ((e = cudaEventCreateWithFlags(&s.h2d_done, cudaEventDisableTiming)) != cudaSuccess ||
+        if ((e = cudaStreamCreateWithFlags(&s.compute, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&s.h2d_done, cudaEventDisableTiming)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&s.compute_done, cudaEventDisableTiming)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&s.d2h_done, cudaEventDisableTiming)) != cudaSuccess ||
             (e = s.kev.create()) != cudaSuccess) {
@@ -549,6 +560,8 @@ void bmc_cuda_destroy(bmc_ctx* ctx) {
         if (s.compute_done) cudaEventDestroy(s.compute_done);
         if (s.d2h_done) cudaEventDestroy(s.d2h_done);
         s.kev.destroy();
+        s.sc.release();
+        if (s.compute) cudaStreamDestroy(s.compute);
     }
     for (bmc::DevBuf* b : {&ctx->d_table, &ctx->d_coarse, &ctx->total_steps, &ctx->draw_ctr, &ctx->partials,
                            &ctx->sel_hist, &ctx->sel_pref, &ctx->sorted_h, &ctx->buckets,
@@ -603,6 +616,23 @@ int bmc_cuda_last_kernel_ms(bmc_ctx* ctx, float* rollout_ms, float* predict_ms) 
     if (ctx->kev.predicted) BMC_CK(ctx, cudaEventElapsedTime(&p, ctx->kev.p0, ctx->kev.p1));
     if (rollout_ms) *rollout_ms = r;
     if (predict_ms) *predict_ms = p;
+    return BMC_OK;
+}
+
+int bmc_cuda_last_stage_ms(bmc_ctx* ctx, float* bin_ms, float* rollout_ms, float* unpermute_ms) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    float b = 0.0f, r = 0.0f, u = 0.0f;
+    BMC_CK(ctx, cudaEventSynchronize(ctx->kev.r1));
+    BMC_CK(ctx, cudaEventElapsedTime(&r, ctx->kev.r0, ctx->kev.r1));
+    if (ctx->kev.predicted) BMC_CK(ctx, cudaEventElapsedTime(&b, ctx->kev.p0, ctx->kev.p1));
+    if (ctx->kev.unpermuted) {
+        BMC_CK(ctx, cudaEventSynchronize(ctx->kev.u1));
+        BMC_CK(ctx, cudaEventElapsedTime(&u, ctx->kev.r1, ctx->kev.u1));
+    }
+    if (bin_ms) *bin_ms = b;
+    if (rollout_ms) *rollout_ms = r;
+    if (unpermute_ms) *unpermute_ms = u;
     return BMC_OK;
 }
 

@@ -56,18 +56,21 @@ struct PinBuf {
     }
 };
 
+// Events around the stages of one rollout launch: binning (p0..p1),
+// rollout (r0..r1), unpermute (r1..u1).
 struct KernelEvents {
-    cudaEvent_t p0 = nullptr, p1 = nullptr, r0 = nullptr, r1 = nullptr;
-    bool predicted = false;
+    cudaEvent_t p0 = nullptr, p1 = nullptr, r0 = nullptr, r1 = nullptr, u1 = nullptr;
+    bool predicted = false, unpermuted = false;
     cudaError_t create() {
         cudaError_t e;
         if ((e = cudaEventCreate(&p0)) != cudaSuccess) return e;
         if ((e = cudaEventCreate(&p1)) != cudaSuccess) return e;
         if ((e = cudaEventCreate(&r0)) != cudaSuccess) return e;
+        if ((e = cudaEventCreate(&u1)) != cudaSuccess) return e;
         return cudaEventCreate(&r1);
     }
     void destroy() {
-        for (cudaEvent_t* ev : {&p0, &p1, &r0, &r1}) {
+        for (cudaEvent_t* ev : {&p0, &p1, &r0, &r1, &u1}) {
             if (*ev) cudaEventDestroy(*ev);
             *ev = nullptr;
         }
@@ -106,7 +109,12 @@ struct Plan {
     float coarse_h = 0.0f;
 };
 
+// One pipeline slot: its own compute stream and rollout scratch, so chunk
+// k+1's binning and rollout fill the SMs chunk k's persistent rollout
+// releases during its tail instead of waiting for the whole kernel.
 struct Slot {
+    cudaStream_t compute = nullptr;
+    Scratch sc;
     PinBuf h_terms, h_out;
     DevBuf d_terms, d_out;
     cudaEvent_t h2d_done = nullptr, compute_done = nullptr, d2h_done = nullptr;

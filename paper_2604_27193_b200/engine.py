@@ -285,6 +285,12 @@ class CudaExecutor:
         self._check(self.lib.bmc_cuda_last_kernel_ms(self.ctx, C.byref(r), C.byref(p)))
         return float(r.value), float(p.value)
 
+    def last_stage_ms(self):
+        """(binning, rollout, unpermute) device ms of the last device-resident rollout."""
+        b, r, u = C.c_float(0), C.c_float(0), C.c_float(0)
+        self._check(self.lib.bmc_cuda_last_stage_ms(self.ctx, C.byref(b), C.byref(r), C.byref(u)))
+        return float(b.value), float(r.value), float(u.value)
+
     def lane_efficiency(self):
         """(executed steps, lane slots, efficiency) of the last rollout launch."""
         a, b = C.c_uint64(0), C.c_uint64(0)
