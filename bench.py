@@ -241,7 +241,7 @@ def device_sampler(bmc, ex, sw, args, model, n, begin, dev_terms, world, dist, c
     torch.cuda.empty_cache()
     out = np.empty(n, dtype=bmc.RESULT_DTYPE)
     ex.run_model(model, n, first=begin, world=sw, out=out, sampler="device")  # warm-up
-    if world > 1:
+    if dist is not None:
         dist.barrier()
     reps = max(1, min(args.steps, 3))
     tt = time.perf_counter()
@@ -249,7 +249,7 @@ def device_sampler(bmc, ex, sw, args, model, n, begin, dev_terms, world, dist, c
         rep, _ = ex.run_model(model, n, first=begin, world=sw, out=out, sampler="device")
     e2e_s = (time.perf_counter() - tt) / reps
     te = torch.tensor([e2e_s, 0.0 if same else 1.0], dtype=torch.float64, device=cdev)
-    if world > 1:
+    if dist is not None:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     return {"available": True, "bit_identical_to_host_draw": float(te[1].item()) == 0.0,
             "verified_samples": n, "clamp_count": dclamps, "draw_s": draw_s,
@@ -326,7 +326,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
 
     from paper_2604_27193_b200 import distributed as D
     cdev = coll_device or f"cuda:{local_rank}"
-    coll = D.Collective(dist if world > 1 else None, cdev)
+    coll = D.Collective(dist, cdev)
 
     class CountingShard(D.DeviceShard):
         """DeviceShard that tallies the kernels each statistic launches."""
@@ -374,7 +374,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     clocks.start()
-    if world > 1:
+    if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -386,12 +386,12 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
         steps_sum += int(total_steps.item())
     ev1.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if dist is not None:
         dist.barrier()
     clk = clocks.stop()
     elapsed_ms = ev0.elapsed_time(ev1)
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=cdev)
-    if world > 1:
+    if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
     value = n_total / (ms_per_step * 1e-3)
@@ -436,7 +436,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
         out = np.empty(n, dtype=bmc.RESULT_DTYPE)
         for _ in range(max(1, args.warmup // 2)):
             ex.run(samples, sw, out=out)
-        if world > 1:
+        if dist is not None:
             dist.barrier()
         tt = time.perf_counter()
         reps = max(1, min(args.steps, 3))
@@ -444,7 +444,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
             rep = ex.run(samples, sw, out=out)
         e2e_s = (time.perf_counter() - tt) / reps
         te = torch.tensor([e2e_s], dtype=torch.float64, device=cdev)
-        if world > 1:
+        if dist is not None:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": n_total / float(te.item()), "unit": "rollouts/s",
                "h2d_bytes_per_step": rep.h2d_bytes, "d2h_bytes_per_step": rep.d2h_bytes,
@@ -520,7 +520,9 @@ def main():
         reference_arm(args, rank)
         return
     dist = None
-    if world > 1:
+    # a process group whenever launched by torchrun (WORLD_SIZE set), also at
+    # N=1, so the scaling run's collective path is the one measured
+    if "WORLD_SIZE" in os.environ:
         import torch
         import torch.distributed as dist
         local_rank = local_rank % max(1, torch.cuda.device_count())

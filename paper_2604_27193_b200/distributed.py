@@ -42,7 +42,8 @@ def shard_range(n_total: int, rank: int, world: int):
 class Collective:
     """Allreduce / allgather of small host vectors over torch.distributed.
     ``device`` is where the staging tensors live ("cuda:k" for NCCL, "cpu"
-    for gloo).  world_size 1 (or dist=None) is a no-op."""
+    for gloo).  dist=None (a single process) is a no-op; a process group of
+    size 1 still runs the collectives (so torchrun at N=1 exercises them)."""
 
     def __init__(self, dist=None, device: str = "cpu"):
         self.dist = dist
@@ -55,7 +56,7 @@ class Collective:
 
     def sum_u64(self, arr) -> np.ndarray:
         arr = np.asarray(arr, dtype=np.uint64)
-        if self.world == 1:
+        if self.dist is None:
             return arr.copy()
         import torch
         assert int(arr.max(initial=0)) < 2 ** 63
@@ -70,7 +71,7 @@ class Collective:
         return self._reduce_f64(x, "max")
 
     def _reduce_f64(self, x: float, op: str) -> float:
-        if self.world == 1:
+        if self.dist is None:
             return float(x)
         import torch
         t = self._t([x], torch.float64)
@@ -80,7 +81,7 @@ class Collective:
     def gather_f64(self, vec) -> np.ndarray:
         """rank-ordered all-gather: returns shape (world, len(vec))."""
         vec = np.asarray(vec, dtype=np.float64)
-        if self.world == 1:
+        if self.dist is None:
             return vec[None, :].copy()
         import torch
         t = self._t(vec, torch.float64)

@@ -76,3 +76,20 @@ def test_b200_arm_two_ranks_gloo():
     assert lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0
     assert lines[0]["config"]["parallelism"] == "shard2"
     assert lines[0]["device_sampler"]["bit_identical_to_host_draw"]
+
+
+@pytest.mark.gpu
+def test_b200_arm_nccl_torchrun_one_rank():
+    # the driver's scaling launch (torchrun, NCCL process group, device_id
+    # bound, collectives on CUDA tensors) at world size 1: every allreduce /
+    # allgather of the merged statistics goes through NCCL on the B200
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
+           "--gpus", "1", "--samples", "2e5", "--steps", "2", "--warmup", "3", "--skip-cpu",
+           "--skip-latency"]
+    env = dict(os.environ)
+    env.pop("BMC_DIST_BACKEND", None)
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    (line,) = _json_lines(p.stdout)
+    assert line["n_gpus"] == 1 and line["value"] > 0 and line["config"]["parallelism"] == "shard1"
