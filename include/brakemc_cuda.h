@@ -251,6 +251,18 @@ int bmc_cuda_summarize(bmc_ctx* ctx, const double* stop_distance, const uint8_t*
  * (any order): counts[j] = #{hit_horizon || d > headways[j]}. */
 int bmc_cuda_exceedance(bmc_ctx* ctx, const double* stop_distance, const uint8_t* hit_horizon,
                         size_t n, const double* headways, size_t m, uint64_t* counts);
+/* Sensor-noise TTC sweep (BASELINE C4; an extension, the reference has no
+ * noise model).  Result i (global sample index first + i) triggers braking
+ * at a measured TTC ttc[j] + eps_i, eps_i = sigma * standard_normal_at(
+ * noise_seed, first + i) -- the reference's Box-Muller (sampling.cpp:48-53)
+ * on its own counter stream -- so counts[j] = #{hit_horizon ||
+ * d > (ttc[j] + eps_i) * closing_speed}.  sigma = 0 equals bmc_cuda_exceedance
+ * at headways ttc[j] * closing_speed.  Needs the device sampler gate
+ * (bmc_device_sampler_available); m <= 1024 thresholds, any order. */
+int bmc_cuda_exceedance_ttc_noise(bmc_ctx* ctx, const double* stop_distance,
+                                  const uint8_t* hit_horizon, size_t n, uint64_t first,
+                                  uint64_t noise_seed, double sigma, const double* ttc, size_t m,
+                                  double closing_speed, uint64_t* counts);
 /* Exact order statistics: out[j] = ranks[j]-th smallest (1-based) value of
  * stop_distance, over non-horizon results only when exclude_horizon != 0.
  * Ranks outside [1, count] give NaN. */

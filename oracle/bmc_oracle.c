@@ -279,6 +279,24 @@ uint64_t orc_exceed_count(const orc_result* r, size_t n, double headway) {
     return c;
 }
 
+/* Sensor-noise TTC sweep (the engine's C4 extension; not in the reference):
+ * eps_i = sigma * standard_normal_at(seed, first + i) (sampling.cpp:48-53),
+ * collision iff hit_horizon || d > (ttc[j] + eps_i) * v.  Plain loops. */
+void orc_exceed_ttc_noise(const orc_result* r, size_t n, uint64_t first, uint64_t seed,
+                          double sigma, const double* ttc, size_t m, double v, uint64_t* counts) {
+    for (size_t j = 0; j < m; ++j) counts[j] = 0;
+    for (size_t i = 0; i < n; ++i) {
+        if (r[i].hit_horizon) {
+            for (size_t j = 0; j < m; ++j) counts[j] += 1u;
+            continue;
+        }
+        const double eps = sigma * orc_standard_normal_at(seed, first + i);
+        for (size_t j = 0; j < m; ++j) {
+            if (r[i].stop_distance > (ttc[j] + eps) * v) counts[j] += 1u;
+        }
+    }
+}
+
 /* analysis.cpp:161-194 -- nudged rank over the finite stoppers */
 int orc_min_safe_headway(const orc_result* r, size_t n, double risk, double* out) {
     if (!(risk > 0.0 && risk < 1.0) || n == 0) {

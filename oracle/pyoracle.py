@@ -304,6 +304,9 @@ class Port:
         L.orc_exceed_count.restype = C.c_uint64
         L.orc_exceed_count.argtypes = [C.c_void_p, C.c_size_t, C.c_double]
         L.orc_min_safe_headway.argtypes = [C.c_void_p, C.c_size_t, C.c_double, _D]
+        L.orc_exceed_ttc_noise.restype = None
+        L.orc_exceed_ttc_noise.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64, C.c_uint64,
+                                           C.c_double, _D, C.c_size_t, C.c_double, _U64]
         L.orc_headway_grid.restype = C.c_long
         L.orc_headway_grid.argtypes = [C.c_double, C.c_double, C.c_double, _D, C.c_size_t]
         L.orc_fine_stopping_distance.restype = C.c_double
@@ -339,6 +342,17 @@ class Port:
         w = _orc_world(world)
         if self.lib.orc_run(_ptr(samples), samples.shape[0], C.byref(w), _ptr(out), threads) != 0:
             raise OracleError("orc_run failed")
+        return out
+
+    def exceed_ttc_noise(self, results, ttc, closing_speed, sigma, noise_seed, first=0):
+        """Sensor-noise TTC sweep counts (orc_exceed_ttc_noise)."""
+        results = np.ascontiguousarray(results, dtype=RESULT_DTYPE)
+        t = np.ascontiguousarray(ttc, dtype=np.float64)
+        out = np.zeros(t.shape[0], dtype=np.uint64)
+        self.lib.orc_exceed_ttc_noise(_ptr(results), results.shape[0], int(first),
+                                      int(noise_seed) & ((1 << 64) - 1), float(sigma),
+                                      _ptr(t, _D), t.shape[0], float(closing_speed),
+                                      _ptr(out, _U64))
         return out
 
     def summarize(self, results, bin_width=2.0):

@@ -149,6 +149,8 @@ SIGNATURES = [
     ("bmc_cuda_summarize", C.c_int, [_P, _P, _P, C.c_size_t, C.c_double, C.POINTER(Summary), _P,
                                      C.c_size_t]),
     ("bmc_cuda_exceedance", C.c_int, [_P, _P, _P, C.c_size_t, _P, C.c_size_t, _P]),
+    ("bmc_cuda_exceedance_ttc_noise", C.c_int, [_P, _P, _P, C.c_size_t, C.c_uint64, C.c_uint64,
+                                                C.c_double, _P, C.c_size_t, C.c_double, _P]),
     ("bmc_cuda_order_stats", C.c_int, [_P, _P, _P, C.c_size_t, C.c_int, _P, C.c_size_t, _P,
                                        C.POINTER(C.c_uint64)]),
     ("bmc_cuda_fp64_peak", C.c_int, [_P, C.c_int, C.POINTER(C.c_double),

@@ -205,6 +205,71 @@ int bmc_cuda_summarize(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t 
     return BMC_OK;
 }
 
+int bmc_cuda_exceedance_ttc_noise(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n,
+                                  uint64_t first, uint64_t noise_seed, double sigma,
+                                  const double* ttc, size_t m, double closing_speed,
+                                  uint64_t* counts) {
+    int rc = bmc::prepare(ctx);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (n == 0) return fail(ctx, BMC_E_CONFIG, "risk: needs at least one result");
+    if (m == 0) return BMC_OK;
+    if (!d || !ttc || !counts) return fail(ctx, BMC_E_CONFIG, "exceedance: null argument");
+    if (!(closing_speed > 0.0)) return fail(ctx, BMC_E_CONFIG, "risk.closing_speed: must be > 0");
+    if (!(sigma >= 0.0) || !std::isfinite(sigma)) {
+        return fail(ctx, BMC_E_CONFIG, "risk.sensor_noise: must be finite and >= 0");
+    }
+    if (m > static_cast<size_t>(bmc::kNoiseMaxThresholds)) {
+        return fail(ctx, BMC_E_RANGE, "risk.ttc: at most 1024 thresholds");
+    }
+    for (size_t j = 0; j < m; ++j) {
+        if (!std::isfinite(ttc[j])) return fail(ctx, BMC_E_CONFIG, "risk.ttc: must be finite");
+    }
+    std::string why;
+    if (!bmc::device_sampler_supported(&why)) {
+        return fail(ctx, BMC_E_CONFIG, "risk.sensor_noise: " + why);
+    }
+    ctx->last_launches = 0;
+    std::vector<size_t> order(m);
+    std::iota(order.begin(), order.end(), size_t{0});
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return ttc[a] < ttc[b]; });
+    std::vector<double> sorted(m);
+    for (size_t j = 0; j < m; ++j) sorted[j] = ttc[order[j]];
+    cudaStream_t s = ctx->stream;
+    BMC_CK(ctx, ctx->sorted_h.reserve(m * sizeof(double)));
+    BMC_CK(ctx, ctx->buckets.reserve((m + 1) * sizeof(unsigned long long)));
+    BMC_CK(ctx, ctx->draw_ctr.reserve(16));
+    BMC_CK(ctx, cudaMemcpyAsync(ctx->sorted_h.p, sorted.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
+    BMC_CK(ctx, cudaMemsetAsync(ctx->buckets.p, 0, (m + 1) * sizeof(unsigned long long), s));
+    BMC_CK(ctx, cudaMemsetAsync(ctx->draw_ctr.p, 0, 16, s));
+    bmc::NoiseExceedArgs a{};
+    a.d = d;
+    a.hz = hz;
+    a.n = n;
+    a.first = first;
+    a.seed = noise_seed;
+    a.sigma = sigma;
+    a.closing = closing_speed;
+    a.ttc = ctx->sorted_h.as<double>();
+    a.m = static_cast<int>(m);
+    a.buckets = ctx->buckets.as<unsigned long long>();
+    a.flags = reinterpret_cast<unsigned int*>(ctx->draw_ctr.as<char>() + 8);
+    BMC_CK(ctx, bmc::launch_noise_exceed(a, ctx->sms, s));
+    std::vector<unsigned long long> b(m + 1);
+    BMC_CK(ctx, cudaMemcpyAsync(b.data(), ctx->buckets.p, (m + 1) * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, s));
+    if ((rc = bmc::finish_draw(ctx, ctx->draw_ctr, nullptr)) != BMC_OK) return rc;  // syncs s
+    ctx->last_launches = 1;
+    uint64_t suffix = 0;
+    std::vector<uint64_t> ex(m);
+    for (size_t j = m; j-- > 0;) {
+        suffix += b[j + 1];
+        ex[j] = suffix;
+    }
+    for (size_t j = 0; j < m; ++j) counts[order[j]] = ex[j];
+    return BMC_OK;
+}
+
 int bmc_cuda_exceedance(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n,
                         const double* headways, size_t m, uint64_t* counts) {
     int rc = bmc::prepare(ctx);

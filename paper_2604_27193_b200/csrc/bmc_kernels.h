@@ -93,6 +93,28 @@ struct DrawArgs {
 };
 cudaError_t launch_draw_terms(const DrawArgs& a, int sms, cudaStream_t s);
 
+// Sensor-noise TTC sweep (C4 extension; the reference has no noise model):
+// sample i's AEB trigger fires at a measured TTC T_j + eps_i with
+// eps_i = sigma * standard_normal_at(noise_seed, first + i) (the reference's
+// Box-Muller on its own counter stream, through the glibc port), so its
+// headway at brake onset is H_ij = (T_j + eps_i) * v_closing and it
+// collides iff hit_horizon or stop_distance > H_ij.  With T sorted
+// ascending, H_ij is non-decreasing in j and bucket p_i = #{j : H_ij < d_i}
+// (m for a horizon hit) gives count_j = #{i : p_i > j}.  sigma = 0 reduces
+// exactly to collision_probability(results, T_j * v) (analysis.cpp:145-159).
+struct NoiseExceedArgs {
+    const double* d;
+    const uint8_t* hz;      // nullable
+    uint64_t n, first, seed;
+    double sigma, closing;
+    const double* ttc;      // device, m sorted ascending
+    int m;
+    unsigned long long* buckets;  // device, m + 1, zeroed
+    unsigned int* flags;          // device, DrawFlags OR-ed
+};
+constexpr int kNoiseMaxThresholds = 1024;
+cudaError_t launch_noise_exceed(const NoiseExceedArgs& a, int sms, cudaStream_t s);
+
 struct LaunchShape {
     int block_threads;
     int grid;

@@ -75,7 +75,61 @@ __global__ void __launch_bounds__(kDrawThreads) draw_terms_kernel(DrawArgs a) {
     }
 }
 
+__global__ void __launch_bounds__(kDrawThreads) noise_exceed_kernel(NoiseExceedArgs a) {
+    __shared__ uint64_t s_log[glibc::kLogTabWords];
+    __shared__ uint64_t s_sct[glibc::kSinCosTabWords];
+    __shared__ double s_t[kNoiseMaxThresholds];
+    __shared__ unsigned int s_b[kNoiseMaxThresholds + 1];
+    for (int i = threadIdx.x; i < glibc::kLogTabWords; i += blockDim.x) s_log[i] = g_log_tab[i];
+    for (int i = threadIdx.x; i < glibc::kSinCosTabWords; i += blockDim.x) s_sct[i] = g_sincos_tab[i];
+    for (int j = threadIdx.x; j < a.m; j += blockDim.x) s_t[j] = a.ttc[j];
+    for (int j = threadIdx.x; j <= a.m; j += blockDim.x) s_b[j] = 0u;
+    __syncthreads();
+    unsigned int flags = 0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
+         i += stride) {
+        int p;
+        if (a.hz && a.hz[i]) {
+            p = a.m;
+        } else {
+            bool bad = false;
+            const double z = glibc::standard_normal_at(a.seed, a.first + i, s_log, s_sct, &bad);
+            if (bad) flags |= kDrawUnported;
+            const double eps = __dmul_rn(a.sigma, z);
+            const double v = a.d[i];
+            int lo = 0, hi = a.m;  // first j with !(H_j < v); H_j = (T_j + eps) * closing
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (__dmul_rn(__dadd_rn(s_t[mid], eps), a.closing) < v) {
+                    lo = mid + 1;
+                } else {
+                    hi = mid;
+                }
+            }
+            p = lo;
+        }
+        atomicAdd(&s_b[p], 1u);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j <= a.m; j += blockDim.x) {
+        if (s_b[j]) atomicAdd(&a.buckets[j], static_cast<unsigned long long>(s_b[j]));
+    }
+    for (int o = 16; o > 0; o >>= 1) flags |= __shfl_xor_sync(0xffffffffu, flags, o);
+    if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.flags, flags);
+}
+
 }  // namespace
+
+cudaError_t launch_noise_exceed(const NoiseExceedArgs& a, int sms, cudaStream_t s) {
+    if (a.n == 0) return cudaSuccess;
+    if (a.m < 1 || a.m > kNoiseMaxThresholds) return cudaErrorInvalidValue;
+    const uint64_t blocks_needed = (a.n + kDrawThreads - 1) / kDrawThreads;
+    const uint64_t cap = static_cast<uint64_t>(sms > 0 ? sms : 148) * 4;
+    const unsigned grid = static_cast<unsigned>(blocks_needed < cap ? blocks_needed : cap);
+    noise_exceed_kernel<<<grid, kDrawThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_draw_terms(const DrawArgs& a, int sms, cudaStream_t s) {
     if (a.n == 0) return cudaSuccess;

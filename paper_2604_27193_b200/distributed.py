@@ -189,6 +189,10 @@ class DeviceShard:
     def select_pass(self, exclude_horizon: bool, shift: int, prefixes) -> np.ndarray:
         return self.ex.select_pass(self.d, self.hz, exclude_horizon, shift, prefixes)
 
+    def exceedance_ttc_noise(self, ttc, closing_speed, sigma, noise_seed, first) -> np.ndarray:
+        return self.ex.exceedance_ttc_noise(self.d, self.hz, ttc, closing_speed, sigma,
+                                            noise_seed, first)
+
 
 # ------------------------------------------------------ merged statistics
 
@@ -260,6 +264,14 @@ def exceedance_counts(shard, coll: Collective, headways) -> np.ndarray:
         if not h >= 0.0:
             raise ValueError("risk.headway: must be >= 0")
     return coll.sum_u64(shard.exceedance(headways))
+
+
+def exceedance_ttc_noise_counts(shard, coll: Collective, ttc, closing_speed: float, sigma: float,
+                                noise_seed: int, first: int) -> np.ndarray:
+    """Sensor-noise TTC sweep over all ranks: each rank's noise draws use its
+    global sample indices (first = its shard start), so the sum equals a
+    single-device run exactly."""
+    return coll.sum_u64(shard.exceedance_ttc_noise(ttc, closing_speed, sigma, noise_seed, first))
 
 
 def min_safe_headways(shard, coll: Collective, n_total: int, risks: Sequence[float]):

@@ -339,6 +339,20 @@ class CudaExecutor:
                                                  n, _p(h), h.shape[0], _p(counts)))
         return counts
 
+    def exceedance_ttc_noise(self, d, hz, ttc: Sequence[float], closing_speed: float,
+                             sigma: float, noise_seed: int, first: int = 0) -> np.ndarray:
+        """Sensor-noise TTC sweep: #{hit_horizon or d > (T + eps_i) * v} per
+        threshold T, eps_i = sigma * standard_normal_at(noise_seed, first + i)."""
+        n = int(d.numel())
+        t = np.ascontiguousarray(ttc, dtype=np.float64)
+        counts = np.zeros(t.shape[0], dtype=np.uint64)
+        self._check(self.lib.bmc_cuda_exceedance_ttc_noise(
+            self.ctx, C.c_void_p(d.data_ptr()),
+            C.c_void_p(hz.data_ptr()) if hz is not None else None, n, int(first),
+            int(noise_seed) & ((1 << 64) - 1), float(sigma), _p(t), t.shape[0],
+            float(closing_speed), _p(counts)))
+        return counts
+
     def order_stats(self, d, hz, ranks: Sequence[int], exclude_horizon: bool):
         n = int(d.numel())
         r = np.ascontiguousarray(ranks, dtype=np.uint64)

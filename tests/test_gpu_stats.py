@@ -109,3 +109,36 @@ def test_order_stats_exact(executor):
         assert v == srt[r - 1]
     vals, _ = executor.order_stats(d, None, [0, 100002], exclude_horizon=False)
     assert np.isnan(vals).all()
+
+
+TTC = [1.0 + 0.25 * k for k in range(21)]
+
+
+@pytest.mark.parametrize("sigma", [0.0, 0.05, 0.3, 1.5])
+def test_sensor_noise_ttc_sweep(ref, executor, readme, mixed, sigma):
+    # BASELINE C4's sensor-noise TTC sweep: device counts equal the C oracle
+    # exactly (same glibc Box-Muller stream); sigma = 0 equals the plain
+    # exceedance counts at T * v (the reference's collision_probability)
+    from oracle.pyoracle import Port
+    port = Port()
+    v = 30.0
+    for res in (readme, mixed):
+        d, hz = device(res)
+        got = executor.exceedance_ttc_noise(d, hz, TTC, v, sigma, noise_seed=7, first=1000)
+        want = port.exceed_ttc_noise(res, TTC, v, sigma, noise_seed=7, first=1000)
+        assert got.tolist() == want.tolist()
+        if sigma == 0.0:
+            assert got.tolist() == executor.exceedance_counts(d, hz, [t * v for t in TTC]).tolist()
+
+
+def test_sensor_noise_ttc_shards_add_up(executor, mixed):
+    # rank shards draw their noise at their global indices: the sum over
+    # shards equals the single-device sweep, bit for bit
+    d, hz = device(mixed)
+    n = d.numel()
+    whole = executor.exceedance_ttc_noise(d, hz, TTC[::-1], 30.0, 0.2, noise_seed=11, first=0)
+    cut = n // 3
+    a = executor.exceedance_ttc_noise(d[:cut], hz[:cut], TTC[::-1], 30.0, 0.2, noise_seed=11, first=0)
+    b = executor.exceedance_ttc_noise(d[cut:], hz[cut:], TTC[::-1], 30.0, 0.2, noise_seed=11,
+                                      first=cut)
+    assert (a + b).tolist() == whole.tolist()

@@ -200,3 +200,26 @@ def test_min_safe_headway_with_horizons(ref, port):
     assert port.min_safe_headway(res, 0.1) == math.inf == ref.min_safe_headway(res, 0.1)
     assert port.min_safe_headway(res, 0.2) == 95.0 == ref.min_safe_headway(res, 0.2)
     assert port.exceed_count(res, 1e9) == 2
+
+
+TTC = [1.0 + 0.25 * k for k in range(21)]
+
+
+def test_sensor_noise_ttc_oracle(ref, port):
+    # the C4 extension's oracle: sigma = 0 is the reference's own
+    # collision_probability at T * v; sigma > 0 follows the reference's
+    # standard_normal_at on the noise stream sample by sample
+    samples, _ = ref.draw_batch(Model.mixed(8), 3000)
+    res, _, _ = ref.run(samples, World(), "parallel")
+    v = 30.0
+    zero = port.exceed_ttc_noise(res, TTC, v, 0.0, noise_seed=99, first=0)
+    want = [int(round(ref.collision_probability(res, t * v) * len(res))) for t in TTC]
+    assert zero.tolist() == want
+    seed, first, sigma = 0xABCDEF, 123456, 0.3
+    got = port.exceed_ttc_noise(res, TTC, v, sigma, noise_seed=seed, first=first)
+    eps = [sigma * ref.standard_normal_at(seed, first + i) for i in range(len(res))]
+    brute = [sum(1 for i in range(len(res))
+                 if res["hit_horizon"][i] or res["stop_distance"][i] > (t + eps[i]) * v)
+             for t in TTC]
+    assert got.tolist() == brute
+    assert got.tolist() != zero.tolist()

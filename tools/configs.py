@@ -16,7 +16,9 @@ C4  mixed-condition, divergence-heavy: wet/icy friction N(0.45, 0.2^2),
     grade +-6 %, 1e6 samples: device-resident rollout time,
     SIMT lane efficiency, horizon share, and the TTC-threshold sweep
     T in {1.0, 1.25, ..., 6.0} s (headway T * 30 m/s) whose counts must equal
-    the reference's collision_probability(results, T * v) * n exactly.
+    the reference's collision_probability(results, T * v) * n exactly; and
+    the same sweep with sensor noise on the trigger TTC (sigma = 0.15 s), equal
+    to the C oracle's counts.
 
 python tools/configs.py [--out profiles/round1_configs.json] [--quick]
 """
@@ -153,6 +155,15 @@ def c4(ref, ex, quick):
     same = bool(np.array_equal(got_d.view(np.uint64), want["stop_distance"].view(np.uint64)))
     sub_counts = ex.exceedance_counts(d[:k], hz[:k], heads)
     ref_counts = [int(round(ref.collision_probability(want, h) * k)) for h in heads]
+    # sensor-noise TTC: trigger at T + eps_i, eps_i ~ N(0, sigma^2) on its own
+    # counter stream (the engine's extension; oracle: oracle/bmc_oracle.c)
+    from oracle.pyoracle import Port
+    sigma, noise_seed = 0.15, m.seed + 0x9E3779B97F4A7C15
+    t0 = time.perf_counter()
+    noisy = ex.exceedance_ttc_noise(d, hz, ttc, v_close, sigma, noise_seed)
+    noisy_ms = 1e3 * (time.perf_counter() - t0)
+    noisy_sub = ex.exceedance_ttc_noise(d[:k], hz[:k], ttc, v_close, sigma, noise_seed)
+    noisy_orc = Port().exceed_ttc_noise(want, ttc, v_close, sigma, noise_seed)
     kms = statistics.median(ms)
     total_steps = int(total.item())
     return {
@@ -166,6 +177,15 @@ def c4(ref, ex, quick):
         "ttc_thresholds_s": ttc, "closing_speed_mps": v_close,
         "exceedance_counts": [int(c) for c in counts],
         "collision_probability": [int(c) / n for c in counts],
+        "sensor_noise_ttc": {
+            "sigma_s": sigma, "noise_seed": noise_seed,
+            "model": "trigger at measured TTC T + eps_i, eps_i = sigma * standard_normal_at("
+                     "noise_seed, i); collision iff horizon or d > (T + eps_i) * v",
+            "exceedance_counts": [int(c) for c in noisy],
+            "collision_probability": [int(c) / n for c in noisy],
+            "wall_ms": noisy_ms,
+            "parity_counts_equal_oracle": [int(c) for c in noisy_sub] == [int(c) for c in noisy_orc],
+        },
         "parity_subset": k, "parity_stop_distance_bitwise": same,
         "parity_counts_equal_reference": [int(c) for c in sub_counts] == ref_counts,
         "reference_run_parallel_rollouts_per_s": k / t_cpu, "host_threads": wc,
