@@ -59,7 +59,7 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--samples", type=float, default=1e8)
     p.add_argument("--seed", type=int, default=3)
-    p.add_argument("--latency-reps", type=int, default=300)
+    p.add_argument("--latency-reps", type=int, default=1000)
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--ref-seconds", type=float, default=150.0)
     p.add_argument("--skip-e2e", action="store_true")
