@@ -114,7 +114,8 @@ typedef struct {
 /* Timing breakdown of one bmc_cuda_run call (seconds). */
 typedef struct {
     double wall_s;        /* whole call: staging + H2D + kernels + D2H + unpack */
-    double kernel_ms;     /* sum of rollout-kernel event times */
+    double kernel_ms;     /* sum of per-chunk rollout event spans (the two pipeline slots run on
+                             their own streams, so spans of neighbouring chunks may overlap) */
     double predict_ms;    /* sum of predictor + binning kernel event times */
     uint64_t total_steps; /* sum of executed RK4 steps (roofline numerator) */
     uint64_t h2d_bytes, d2h_bytes;
