@@ -473,17 +473,10 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
     }
     const unsigned lane = threadIdx.x & 31u;
     unsigned long long my_steps = 0, my_slots = 0;
-    for (unsigned iter = 0;; ++iter) {
+    for (;;) {
         unsigned g = 0;
-        if (A.static_groups) {
-            // small batch: warp w of CTA c owns group w * gridDim.x + c, so the
-            // longest groups (sorted first) land one per SM sub-partition
-            if (iter > 0) break;
-            g = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-        } else {
-            if (lane == 0) g = atomicAdd(A.work_counter, 1u);
-            g = __shfl_sync(0xffffffffu, g, 0);
-        }
+        if (lane == 0) g = atomicAdd(A.work_counter, 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
         const uint64_t base = static_cast<uint64_t>(g) * (32u * ILP);
         if (base >= A.n) break;
         if (ILP == 2) {
@@ -709,31 +702,20 @@ cudaError_t launch_rollout_t(const RolloutArgs& a, cudaStream_t s) {
         &per_sm, rollout_kernel<MODE, BT, ILP, UNR>, BT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    // Persistent grid.  Small batches (the real-time case), whose groups all
-    // fit in one wave, spread over every SM with narrower CTAs and a static
-    // group -> warp map: group g runs on warp g / sms of CTA g % sms, so the
-    // longest groups (the binned order puts them first) sit one per SM
-    // sub-partition and their dependent RK4 chains do not share an FP64 pipe.
+    // Persistent grid.  Small batches (the real-time case) spread their
+    // sample groups over every SM with narrower CTAs instead of packing
+    // them into a few full ones: fewer warps per SM = shorter per-step
+    // latency of each dependent RK4 chain.
     const uint64_t groups = (a.n + 32 * ILP - 1) / (32 * ILP);
     const uint64_t sms = static_cast<uint64_t>(sm_count_cached(dev));
     const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
     uint64_t warps_per_block = BT / 32;
-    if (groups <= sms * warps_per_block) {
-        RolloutArgs b = a;
-        b.static_groups = 1;
-        const uint64_t grid = std::min(groups, sms);
-        const uint64_t wpb = (groups + grid - 1) / grid;
-        rollout_kernel<MODE, BT, ILP, UNR><<<static_cast<int>(grid), static_cast<int>(wpb * 32), smem, s>>>(b);
-        return cudaGetLastError();
-    }
     if (groups < resident * warps_per_block) {
         warps_per_block = std::max<uint64_t>(1, (groups + resident - 1) / resident);
     }
     const uint64_t need = (groups + warps_per_block - 1) / warps_per_block;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(need, resident)));
-    RolloutArgs b = a;
-    b.static_groups = 0;
-    rollout_kernel<MODE, BT, ILP, UNR><<<grid, static_cast<int>(warps_per_block * 32), smem, s>>>(b);
+    rollout_kernel<MODE, BT, ILP, UNR><<<grid, static_cast<int>(warps_per_block * 32), smem, s>>>(a);
     return cudaGetLastError();
 }
 

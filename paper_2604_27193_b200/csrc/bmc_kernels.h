@@ -43,7 +43,6 @@ struct RolloutArgs {
     uint8_t* hit_horizon;  // nullable
     unsigned long long* total_steps;  // nullable
     unsigned int* work_counter;       // device, zeroed before launch
-    int32_t static_groups;            // set by the launcher: one group per warp, no counter
     unsigned long long* counters;     // nullable: [0] executed steps, [1] lane slots
     const PackedTerms* packed_in;     // nullable: sorted packed inputs (binned schedule)
     PackedOut* packed_out;            // nullable: sorted packed outputs (binned schedule)
