@@ -174,6 +174,26 @@ public:
         return static_cast<double>(c) / static_cast<double>(n_);
     }
 
+    /// Collision probability per trigger TTC with sensor noise (BASELINE C4;
+    /// an extension -- the reference has no noise model): sample i triggers
+    /// at ttc + eps_i, eps_i = sigma * standard_normal_at(noise_seed, first_index + i)
+    /// (sampling.cpp:48-53 on its own counter stream), and collides iff it
+    /// hits the horizon or stops beyond (ttc + eps_i) * closing_speed.
+    /// sigma = 0 gives collision_probability(ttc * closing_speed) exactly.
+    std::vector<double> collision_probability_ttc_noise(const std::vector<double>& ttc,
+                                                        double closing_speed, double sigma,
+                                                        uint64_t noise_seed,
+                                                        uint64_t first_index = 0) const {
+        std::vector<uint64_t> c(ttc.size());
+        check(bmc_cuda_exceedance_ttc_noise(ctx_, dd(), hzp(), n_, first_index, noise_seed, sigma,
+                                            ttc.data(), ttc.size(), closing_speed, c.data()));
+        std::vector<double> p(ttc.size());
+        for (std::size_t j = 0; j < ttc.size(); ++j) {
+            p[j] = static_cast<double>(c[j]) / static_cast<double>(n_);
+        }
+        return p;
+    }
+
     /// min_safe_headway (analysis.cpp:161-194)
     double min_safe_headway(double risk) const { return min_safe_headways({risk})[0]; }
 

@@ -159,6 +159,18 @@ int main(int argc, char** argv) {
             cp = cp && run.collision_probability(h) == collision_probability(ref.results, h);
         }
         check(cp, "collision_probability exact");
+        // sensor-noise TTC sweep: sigma = 0 is the reference's collision_probability at T * v;
+        // a noisy sweep is monotone in T and shards (first_index) add up to the whole
+        std::vector<double> ttc;
+        for (int k = 0; k <= 20; ++k) ttc.push_back(1.0 + 0.25 * k);
+        const std::vector<double> p0 = run.collision_probability_ttc_noise(ttc, 30.0, 0.0, 17);
+        bool tn = true;
+        for (std::size_t j = 0; j < ttc.size(); ++j) {
+            tn = tn && p0[j] == collision_probability(ref.results, ttc[j] * 30.0);
+        }
+        const std::vector<double> pn = run.collision_probability_ttc_noise(ttc, 30.0, 0.25, 17);
+        for (std::size_t j = 1; j < ttc.size(); ++j) tn = tn && pn[j] <= pn[j - 1];
+        check(tn, "sensor-noise TTC sweep: sigma = 0 equals collision_probability, noisy sweep monotone");
         bool msh = true;
         for (double r : {0.5, 0.3, 0.28, 0.05, 0.01, 0.001}) {
             const double a = run.min_safe_headway(r), bref = min_safe_headway(ref.results, r);

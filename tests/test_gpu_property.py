@@ -88,3 +88,35 @@ def test_random_loop_variants_bit_exact(ref, executor, w, m, n, opts):
     sw = bmc.SimWorld(*w.as_array().tolist())
     got = executor.run(samples, sw, **opts).results
     assert results_bitwise_equal(want, got), opts
+
+
+@settings(max_examples=20, deadline=None, suppress_health_check=list(HealthCheck))
+@given(m=models, first=st.integers(0, 2**40), n=st.integers(1, 20000))
+def test_random_device_draws_bit_exact(executor, m, first, n):
+    # the glibc-port device sampler vs the host pool (itself pinned to the
+    # reference's draw_batch) on random models and index windows
+    if not bmc.device_sampler_available():
+        pytest.skip("device sampler gate closed on this host")
+    model = bmc.UncertaintyModel(m.seed, *zip(m.mean, m.sd))
+    terms, samples, clamps = executor.draw_device(model, n, first=first)
+    host, hclamps = bmc.draw_batch(model, n, first=first)
+    assert np.array_equal(samples.cpu().numpy().view(np.uint64),
+                          np.ascontiguousarray(host).view(np.uint64).reshape(n, 5))
+    assert clamps == hclamps
+    assert np.array_equal(terms.cpu().numpy().view(np.uint64), bmc.stage_terms(host).view(np.uint64))
+
+
+@settings(max_examples=20, deadline=None, suppress_health_check=list(HealthCheck))
+@given(m=models, n=st.integers(1, 4000), sigma=st.floats(0.0, 3.0),
+       seed=st.integers(0, 2**64 - 1), first=st.integers(0, 2**40),
+       ttc=st.lists(st.floats(0.0, 8.0), min_size=1, max_size=40))
+def test_random_sensor_noise_sweeps(ref, executor, m, n, sigma, seed, first, ttc):
+    import torch
+    from oracle.pyoracle import Port
+    samples, _ = ref.draw_batch(m, n)
+    res, _, _ = ref.run(samples, World(), "parallel")
+    d = torch.from_numpy(np.ascontiguousarray(res["stop_distance"])).cuda()
+    hz = torch.from_numpy(np.ascontiguousarray(res["hit_horizon"])).cuda()
+    got = executor.exceedance_ttc_noise(d, hz, ttc, 27.5, sigma, seed, first)
+    want = Port().exceed_ttc_noise(res, ttc, 27.5, sigma, seed, first)
+    assert got.tolist() == want.tolist()
