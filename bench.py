@@ -65,6 +65,7 @@ def parse():
     p.add_argument("--skip-e2e", action="store_true")
     p.add_argument("--skip-latency", action="store_true")
     p.add_argument("--skip-cpu", action="store_true")
+    p.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period (0: off)")
     return p.parse_args()
 
 
@@ -75,17 +76,20 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 200):
         self.index = index
+        self.period_ms = period_ms
         self.rows = []
         self.proc = None
         self.thread = None
 
     def start(self):
+        if self.period_ms <= 0:
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.index)],
+                 "-lms", str(self.period_ms), "-i", str(self.index)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -372,7 +376,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(local_rank, args.clock_ms)
     clocks.start()
     if dist is not None:
         dist.barrier()
