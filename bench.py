@@ -327,6 +327,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     launches = [0]
     kernel_ms = []
     stage_ms = []
+    stats_host_ms = []
 
     from paper_2604_27193_b200 import distributed as D
     cdev = coll_device or f"cuda:{local_rank}"
@@ -367,10 +368,12 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
             stage_ms.append((b_ms, u_ms))
         launches[1] = 0
         # statistics merged over all ranks (one allreduce per quantity)
+        h0 = time.perf_counter()
         counts = D.exceedance_counts(shard, coll, headways)
         summ = D.summarize(shard, coll, 2.0)
         if record:
             launches[0] += nl + launches[1]
+            stats_host_ms.append(1e3 * (time.perf_counter() - h0))
         return counts, summ
 
     for _ in range(args.warmup):
@@ -502,6 +505,9 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
                                         "(MEASURED_PEAKS.json has no FP64 entry)",
                          "spec_peak_tflops": SPEC_FP64_OPS / 1e12},
             "hbm_streams": hbm_streams,
+            "step_breakdown_ms": {"binning": bin_ms, "rollout": roll_ms, "unpermute": unp_ms,
+                                  "statistics_wall": sum(stats_host_ms) / len(stats_host_ms),
+                                  "step": ms_per_step},
             "e2e": e2e,
             "device_sampler": dsamp,
             "latency_25k": latency,
