@@ -24,6 +24,7 @@ bmc_cuda_run_model with the device sampler (sampling included, the
 convention of the reference's feasibility search, analysis.cpp:331-338).
 """
 import argparse
+import gc
 import json
 import math
 import os
@@ -386,6 +387,10 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    # the statistics are host-driven (a few small round trips per step): keep
+    # the collector from pausing the host between them in the timed region
+    gc.collect()
+    gc.disable()
     ev0.record(stream)
     steps_sum = 0
     for _ in range(args.steps):
@@ -393,6 +398,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
         steps_sum += int(total_steps.item())
     ev1.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     if dist is not None:
         dist.barrier()
     clk = clocks.stop()
