@@ -204,6 +204,8 @@ def realtime(bmc, ex, sw, args):
                 g.run(b)
             g.run_model(bmc.UncertaintyModel(seed=999))  # first call captures its graph
         sim_ms, full_ms, steps = [], [], []
+        gc.collect()
+        gc.disable()  # the engine's decision latency, not the interpreter's collector
         for k in range(args.latency_reps):
             t1 = time.perf_counter()
             rep = g.run(batches[k % len(batches)])
@@ -213,6 +215,7 @@ def realtime(bmc, ex, sw, args):
             t1 = time.perf_counter()
             g.run_model(bmc.UncertaintyModel(seed=1000 + k))
             full_ms.append(1e3 * (time.perf_counter() - t1))
+        gc.enable()
         return {"samples": n, "budget_ms": 530.0, "mode": "CUDA graph (H2D, bin, rollout, D2H)",
                 "with_sampling_mode": "CUDA graph (%s)" % (
                     "device sampler: params H2D, draw, bin, rollout, D2H"
@@ -451,11 +454,14 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
             ex.run(samples, sw, out=out)
         if dist is not None:
             dist.barrier()
+        gc.collect()
+        gc.disable()
         tt = time.perf_counter()
         reps = max(1, min(args.steps, 3))
         for _ in range(reps):
             rep = ex.run(samples, sw, out=out)
         e2e_s = (time.perf_counter() - tt) / reps
+        gc.enable()
         te = torch.tensor([e2e_s], dtype=torch.float64, device=cdev)
         if dist is not None:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
