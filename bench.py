@@ -252,10 +252,13 @@ def device_sampler(bmc, ex, sw, args, model, n, begin, dev_terms, world, dist, c
     if dist is not None:
         dist.barrier()
     reps = max(1, min(args.steps, 3))
+    gc.collect()
+    gc.disable()
     tt = time.perf_counter()
     for _ in range(reps):
         rep, _ = ex.run_model(model, n, first=begin, world=sw, out=out, sampler="device")
     e2e_s = (time.perf_counter() - tt) / reps
+    gc.enable()
     te = torch.tensor([e2e_s, 0.0 if same else 1.0], dtype=torch.float64, device=cdev)
     if dist is not None:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
