@@ -67,6 +67,9 @@ def parse():
     p.add_argument("--skip-latency", action="store_true")
     p.add_argument("--skip-cpu", action="store_true")
     p.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period (0: off)")
+    p.add_argument("--parity-samples", type=float, default=2e5,
+                   help="random indices of the timed batch re-simulated by the reference")
+    p.add_argument("--skip-parity", action="store_true")
     return p.parse_args()
 
 
@@ -191,19 +194,27 @@ def _pct(v, p):
     return float(np.percentile(np.array(v), p))
 
 
-def realtime(bmc, ex, sw, args):
+def realtime(bmc, ex, sw, args, headways, risks):
     """C2: 25k-sample decision batches through the CUDA-graph mode, p50/p99
-    over replays on fresh seeds; sim-only (samples given) and with sampling
-    (host pool draws inside the decision, analysis.cpp:331-338)."""
+    over replays on fresh seeds: sim-only (samples given, per-sample results
+    back), with the fused statistics stage in the graph (P(collision) per TTC
+    threshold + min_safe_headway per decision), and with sampling inside the
+    decision as well (the reference's feasibility convention,
+    analysis.cpp:331-338)."""
+    from paper_2604_27193_b200.stats import StatsRequest
     n = 25000
+    req = StatsRequest(headways=headways, risk_levels=risks)
     g = ex.graph(n, sw)
+    gs = ex.graph(n, sw, stats=req)
     try:
         batches = [bmc.draw_batch(bmc.UncertaintyModel(seed=s), n)[0] for s in range(1, 17)]
         for _ in range(2):
             for b in batches:
                 g.run(b)
-            g.run_model(bmc.UncertaintyModel(seed=999))  # first call captures its graph
-        sim_ms, full_ms, steps = [], [], []
+                gs.run(b)
+                gs.stats()
+            gs.run_model(bmc.UncertaintyModel(seed=999))  # first call captures its graph
+        sim_ms, st_ms, full_ms, steps = [], [], [], []
         gc.collect()
         gc.disable()  # the engine's decision latency, not the interpreter's collector
         for k in range(args.latency_reps):
@@ -213,21 +224,36 @@ def realtime(bmc, ex, sw, args):
             steps.append(int(rep.results["steps"].max()))
         for k in range(args.latency_reps):
             t1 = time.perf_counter()
-            g.run_model(bmc.UncertaintyModel(seed=1000 + k))
+            gs.run(batches[k % len(batches)])
+            dec = gs.stats()
+            st_ms.append(1e3 * (time.perf_counter() - t1))
+        for k in range(args.latency_reps):
+            t1 = time.perf_counter()
+            gs.run_model(bmc.UncertaintyModel(seed=1000 + k))
+            gs.stats()
             full_ms.append(1e3 * (time.perf_counter() - t1))
         gc.enable()
         return {"samples": n, "budget_ms": 530.0, "mode": "CUDA graph (H2D, bin, rollout, D2H)",
-                "with_sampling_mode": "CUDA graph (%s)" % (
+                "with_sampling_mode": "CUDA graph (%s) + statistics stage" % (
                     "device sampler: params H2D, draw, bin, rollout, D2H"
                     if bmc.device_sampler_available() else "host sampler, terms H2D"),
                 "sim_only_ms": {"p50": _pct(sim_ms, 50), "p99": _pct(sim_ms, 99),
                                 "reps": len(sim_ms)},
+                "with_statistics_ms": {"p50": _pct(st_ms, 50), "p99": _pct(st_ms, 99),
+                                       "reps": len(st_ms),
+                                       "returns": "per-sample results + collision probability at "
+                                                  "%d TTC thresholds + min_safe_headway at %s"
+                                                  % (len(headways), risks)},
                 "with_sampling_ms": {"p50": _pct(full_ms, 50), "p99": _pct(full_ms, 99),
                                      "reps": len(full_ms)},
+                "last_decision_collision_probability": [float(x) for x in
+                                                        dec["collision_probability"]],
                 "longest_rollout_steps_p50": _pct(steps, 50),
-                "kernel_launches_per_decision": rep.launches}
+                "kernel_launches_per_decision": rep.launches,
+                "kernel_launches_per_decision_with_statistics": dec["launches"]}
     finally:
         g.close()
+        gs.close()
 
 
 def device_sampler(bmc, ex, sw, args, model, n, begin, dev_terms, world, dist, cdev):
@@ -301,6 +327,82 @@ def feasibility_search(bmc, ex, sw, args):
                 else "host sampler -> pinned SoA -> H2D, overlapped")}
 
 
+def parity_spot_check(bmc, args, samples, begin, d, st, hz, sw, out, dist, cdev, headways,
+                      risks):
+    """Checker leg (after the timed region): the headline run's own outputs
+    against the reference.  (1) `--parity-samples` random indices of this
+    rank's shard re-simulated by the unmodified reference (oracle/_ref,
+    run_parallel) and compared bit for bit on all of (stop_distance, steps,
+    hit_horizon); (2) at N=1 the step's statistics against a host recount
+    over the full per-sample outputs with the reference's formulas
+    (analysis.cpp:13-76, 145-194)."""
+    import torch
+    from oracle.pyoracle import Reference, World
+    n = samples.shape[0]
+    k = int(min(n, args.parity_samples))
+    rng = np.random.default_rng(20261017 + begin)
+    idx = np.sort(rng.choice(n, size=k, replace=False)) if k < n else np.arange(n)
+    ti = torch.from_numpy(idx).to(d.device)
+    gd = d.index_select(0, ti).cpu().numpy()
+    gs = st.index_select(0, ti).cpu().numpy()
+    gh = hz.index_select(0, ti).cpu().numpy()
+    t0 = time.perf_counter()
+    ref = Reference()
+    want, _, _ = ref.run(np.ascontiguousarray(samples[idx]), World(), "parallel", 0)
+    ref_s = time.perf_counter() - t0
+    mism = int(np.count_nonzero((gd.view(np.uint64) != want["stop_distance"].view(np.uint64)) |
+                                (gs.astype(np.int64) != want["steps"]) |
+                                (gh.astype(np.uint8) != want["hit_horizon"].astype(np.uint8))))
+    te = torch.tensor([mism, k], dtype=torch.int64, device=cdev)
+    if dist is not None:
+        dist.all_reduce(te)
+    res = {"rollouts_checked": int(te[1].item()), "rollout_mismatches": int(te[0].item()),
+           "rollout_checker": "oracle/_ref run_parallel on random indices of the timed batch "
+                              f"({ref_s:.1f} s on rank 0)"}
+    if dist is None or dist.get_world_size() == 1:
+        # statistics recount over all n outputs (integer / order quantities exact)
+        t1 = time.perf_counter()
+        hd = d.cpu().numpy()
+        hh = hz.cpu().numpy() != 0
+        bad = []
+        hs = np.sort(np.asarray(headways))
+        p = np.searchsorted(hs, hd, side="left")  # #{h < d}
+        p[hh] = len(hs)
+        cnt = np.bincount(p, minlength=len(hs) + 1)
+        ex = np.cumsum(cnt[::-1])[::-1][1:]  # #{p > j}
+        if not np.array_equal(ex.astype(np.uint64), out["exceed"][np.argsort(np.argsort(headways))]):
+            bad.append("exceed")
+        sm = out["summary"]
+        if sm["horizon_count"] != int(hh.sum()):
+            bad.append("horizon_count")
+        if sm["min"] != float(hd.min()) or sm["max"] != float(hd.max()):
+            bad.append("extrema")
+        lo, hi = math.floor(hd.min()), math.ceil(hd.max())
+        bins = max(1, int(math.ceil((hi - lo) / 2.0)))
+        hidx = np.minimum(((hd - lo) / 2.0).astype(np.uint64), np.uint64(bins - 1))
+        if not np.array_equal(np.bincount(hidx.astype(np.int64), minlength=bins).astype(np.uint64),
+                              sm["histogram"]):
+            bad.append("histogram")
+        srt = np.partition(hd, [n // 2 - 1, n // 2])
+        med = srt[n // 2] if n % 2 else 0.5 * (srt[n // 2 - 1] + srt[n // 2])
+        if sm["median"] != med:
+            bad.append("median")
+        stopped = hd[~hh]
+        for r, v in zip(risks, out["min_safe_headway"]):
+            raw = (1.0 - r) * float(n)
+            rank = int(math.ceil(raw - raw * 1e-12))
+            w = math.inf if rank > stopped.size else float(np.partition(stopped, rank - 1)[rank - 1])
+            if v != w:
+                bad.append(f"min_safe_headway({r})")
+        res.update({"statistics_recount": "exceedance counts, horizon count, min/max, histogram, "
+                                          "median, min_safe_headway: host recount over all "
+                                          f"{n} outputs with the reference formulas",
+                    "statistics_mismatches": bad,
+                    "mean_rel_dev_vs_numpy": abs(sm["mean"] - float(hd.mean())) / abs(sm["mean"]),
+                    "recount_s": time.perf_counter() - t1})
+    return res
+
+
 def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     import torch
     import paper_2604_27193_b200 as bmc
@@ -331,6 +433,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     # C4-style TTC threshold sweep: T in {1.0, 1.25, ..., 6.0} s, closing 30 m/s
     ttc = [1.0 + 0.25 * k for k in range(21)]
     headways = [t * model.initial_speed[0] for t in ttc]
+    risks = [0.05, 0.01, 0.001]
     launches = [0]
     kernel_ms = []
     stage_ms = []
@@ -338,50 +441,30 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
 
     from paper_2604_27193_b200 import distributed as D
     cdev = coll_device or f"cuda:{local_rank}"
-    coll = D.Collective(dist, cdev)
-
-    class CountingShard(D.DeviceShard):
-        """DeviceShard that tallies the kernels each statistic launches."""
-
-        def _n(self, r):
-            launches[1] += self.ex.last_launches()
-            return r
-
-        def partials(self):
-            return self._n(super().partials())
-
-        def moments(self, mean):
-            return self._n(super().moments(mean))
-
-        def histogram(self, origin, bw, bins):
-            return self._n(super().histogram(origin, bw, bins))
-
-        def exceedance(self, headways):
-            return self._n(super().exceedance(headways))
-
-        def select_pass(self, exclude, shift, prefixes):
-            return self._n(super().select_pass(exclude, shift, prefixes))
-
-    shard = CountingShard(ex, d, hz)
-    launches.append(0)
+    merge = None
+    if dist is not None:
+        merge = D.TorchMerge(dist, f"cuda:{local_rank}", via_host=(cdev == "cpu"))
+    # the fused statistics stage: pass 1 in the rollout epilogue, then one
+    # streaming pass + compaction + selection (3 merge points under torchrun)
+    stage = ex.stats_stage(n, headways, risks, summarize=True, bin_width=2.0)
+    last = {}
 
     def step(record=False):
         total_steps.zero_()
-        ex.rollout_device(dev_terms, (d, st, hz), sw, total_steps=total_steps)
+        stage.begin()
+        ex.rollout_device(dev_terms, (d, st, hz), sw, total_steps=total_steps, stats=stage)
         nl = ex.last_launches()
         if record:
             b_ms, r_ms, u_ms = ex.last_stage_ms()
             kernel_ms.append(r_ms)
             stage_ms.append((b_ms, u_ms))
-        launches[1] = 0
-        # statistics merged over all ranks (one allreduce per quantity)
         h0 = time.perf_counter()
-        counts = D.exceedance_counts(shard, coll, headways)
-        summ = D.summarize(shard, coll, 2.0)
+        out = stage.finish(d, hz, merge=merge)
         if record:
-            launches[0] += nl + launches[1]
+            launches[0] += nl + out["launches"]
             stats_host_ms.append(1e3 * (time.perf_counter() - h0))
-        return counts, summ
+        last["out"] = out
+        return out
 
     for _ in range(args.warmup):
         step()
@@ -393,14 +476,14 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    # the statistics are host-driven (a few small round trips per step): keep
-    # the collector from pausing the host between them in the timed region
+    # the statistics end in a host read back per step: keep the collector
+    # from pausing the host inside the timed region
     gc.collect()
     gc.disable()
     ev0.record(stream)
     steps_sum = 0
     for _ in range(args.steps):
-        vec, summ = step(record=True)
+        step(record=True)
         steps_sum += int(total_steps.item())
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -415,6 +498,11 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     ms_per_step = float(t.item()) / args.steps
     value = n_total / (ms_per_step * 1e-3)
 
+    parity = None
+    if not args.skip_parity:
+        parity = parity_spot_check(bmc, args, samples, begin, d, st, hz, sw, last["out"], dist,
+                                   cdev, headways, risks)
+    stats_out = last["out"]
     roll_ms = sum(kernel_ms) / len(kernel_ms)
     traffic, traffic_detail = None, None
     tpath = os.path.join(ROOT, "profiles", "rollout_traffic.json")
@@ -484,7 +572,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     latency = None
     feasibility = None
     if rank == 0 and not args.skip_latency:
-        latency = realtime(bmc, ex, sw, args)
+        latency = realtime(bmc, ex, sw, args, headways, risks)
         feasibility = feasibility_search(bmc, ex, sw, args)
 
     cpu = None
@@ -500,25 +588,55 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
             "data": "synthetic (host draw_batch, default UncertaintyModel, bit-identical to "
                     "the reference sampler)",
             "config": {"workload": "C5: %d default-model samples (seed %d), contiguous index "
-                                   "shards per GPU; per step: bin + RK4 rollout + exceedance "
-                                   "counts (21 TTC thresholds) + summarize + allreduce"
-                                   % (n_total, args.seed),
+                                   "shards per GPU; per step: bin + RK4 rollout with statistics "
+                                   "pass 1 fused in its epilogue + statistics stage (21 TTC "
+                                   "exceedance counts, summarize, 3 min_safe_headway levels) + "
+                                   "merge across ranks" % (n_total, args.seed),
                        "samples": n_total, "dt": sw.dt, "t_max": sw.t_max,
                        "parallelism": f"shard{world}",
                        "l2": "no flush: inputs 32 B/sample = %.2f GB per GPU >> 126 MB L2"
                              % (32 * n / 1e9),
                        "sampling_s": sample_s, "clamp_count": clamps},
-            "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
-                         "unit": "TFLOP/s", "frac": achieved / peak_ops, "traffic": traffic,
+            "roofline": {"bound": "fp64", "achieved": executed / 1e12, "peak": peak_ops / 1e12,
+                         "unit": "TFLOP/s", "frac": executed / peak_ops, "traffic": traffic,
                          "traffic_detail": traffic_detail,
+                         "basis": "FP64 ops the kernel executes (DADD/DMUL/DFMA, %d per RK4 "
+                                  "step) x RK4 steps executed in the launch (kernel counter) / "
+                                  "rollout-kernel CUDA-event time on its stream"
+                                  % EXEC_FLOPS_PER_STEP,
                          "kernel": "rollout_kernel", "kernel_ms": roll_ms,
                          "rk4_steps_per_launch": steps_per_launch,
-                         "algorithmic_flops_per_step": ALGO_FLOPS_PER_STEP,
                          "executed_flops_per_step": EXEC_FLOPS_PER_STEP,
-                         "executed_frac": executed / peak_ops,
+                         "algorithmic_equivalent": {
+                             "flops_per_step": ALGO_FLOPS_PER_STEP,
+                             "tflops": achieved / 1e12, "ratio_to_peak": achieved / peak_ops,
+                             "note": "SURVEY 8d counts 57 FP64 ops per step in the reference "
+                                     "formulation; the exact per-batch actuator table (-21) and "
+                                     "exact-doubling FMAs (-4) leave 32 executed, so this ratio "
+                                     "is not a pipe fraction and may exceed 1"},
                          "peak_source": "measured in-run: unfused DADD/DMUL probe "
                                         "(MEASURED_PEAKS.json has no FP64 entry)",
                          "spec_peak_tflops": SPEC_FP64_OPS / 1e12},
+            "parity": parity,
+            "statistics": {
+                "stage": "pass 1 fused into the rollout epilogue (per-CTA shared-memory partials: "
+                         "count, horizon, extrema keys, exact sum, exceedance buckets); pass 2 "
+                         "(exact m2/m3, histogram, order-statistic buckets); compaction + exact "
+                         "selection; merges: %s" % ("torch.distributed (%s)" % (
+                             "gloo via host" if cdev == "cpu" else "NCCL")
+                                                    if dist is not None else "none (1 process)"),
+                "stage_kernels_per_step": stats_out["launches"],
+                "fallbacks": stats_out["fallbacks"],
+                "merge_calls_per_step": (merge.calls // max(1, args.steps + args.warmup)
+                                         if merge is not None else 0),
+                "n": stats_out["n"], "horizon_count": stats_out["horizon_count"],
+                "ttc_s": ttc,
+                "collision_probability": [float(x) for x in stats_out["collision_probability"]],
+                "risk_levels": risks,
+                "min_safe_headway_m": [float(x) for x in stats_out["min_safe_headway"]],
+                "mean": stats_out["summary"]["mean"], "sd": stats_out["summary"]["sd"],
+                "median": stats_out["summary"]["median"],
+                "skewness": stats_out["summary"]["skewness"]},
             "hbm_streams": hbm_streams,
             "step_breakdown_ms": {"binning": bin_ms, "rollout": roll_ms, "unpermute": unp_ms,
                                   "statistics_wall": sum(stats_host_ms) / len(stats_host_ms),
@@ -532,6 +650,7 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
             "gpu_launches": launches[0],
         }
         print(json.dumps(line), flush=True)
+    stage.close()
     ex.close()
 
 

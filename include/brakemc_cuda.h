@@ -297,6 +297,109 @@ int bmc_cuda_select_pass(bmc_ctx* ctx, const double* stop_distance, const uint8_
                          size_t n, int exclude_horizon, int shift, const uint64_t* prefixes,
                          size_t m, uint64_t* hist);
 
+/* --------------------------------------------- fused statistics stage */
+/* The statistics of analysis.cpp computed by a fixed device pipeline that
+ * fuses its first pass into the rollout epilogue (SURVEY.md 8b's
+ * bmc_stats / bmc_stats_req arguments of the rollout call):
+ *   pass 1 (rollout epilogue, per-CTA shared-memory partials, one atomic
+ *           flush per CTA): count, horizon count, min/max (order keys), the
+ *           EXACT sum of stop distances, exceedance counts for the sorted
+ *           headway grid (collision_probability :145-159, build_risk_curve
+ *           :203-228);
+ *   pass 2 (one streaming pass): exact m2/m3 about the mean, the summarize
+ *           histogram (:59-75), level-1 order-statistic histograms;
+ *   compact + select: exact median (:51-57) and min_safe_headway
+ *           (:161-194) from the values of the bucket holding each rank.
+ * Counts, extrema, histogram and order statistics are exact; the sums are
+ * exact and rounded once, so every field is independent of order, chunking
+ * and GPU count (the reference's sequential sum is within (n-1) eps sum|d|).
+ * With no merge the stage has no host round trip before its final read, so
+ * a CUDA graph captures it (bmc_cuda_graph_create_stats). */
+typedef struct {
+    const double* headways;     /* collision thresholds, any order, each >= 0 (nullable if 0) */
+    size_t n_headways;
+    const double* risk_levels;  /* min_safe_headway levels in (0,1), at most 16 (nullable if 0) */
+    size_t n_risk;
+    int32_t summarize;          /* 1: full summarize (moments, median, histogram) */
+    int32_t pad_;
+    double bin_width;           /* summarize histogram width (> 0 when summarize) */
+    uint64_t hist_cap;          /* device histogram capacity in bins; 0 = 8192 (more bins
+                                   take one exact follow-up pass) */
+    uint64_t cand_cap;          /* order-statistic candidates per target; 0 = default
+                                   (max(2^16, max_n/256)); overflow takes the exact
+                                   multi-pass fallback -- results never depend on it */
+} bmc_stats_req;
+
+typedef struct {
+    uint64_t n, horizon_count;
+    bmc_summary summary;        /* valid when the request summarizes */
+    uint64_t* exceed;           /* caller array [n_headways] (nullable): #{hit_horizon || d > h} */
+    double* min_safe_headway;   /* caller array [n_risk] (nullable); +inf in the horizon tail */
+    uint64_t* histogram;        /* caller array (nullable), at least summary.bins entries */
+    size_t histogram_cap;
+    uint32_t launches;          /* kernels the stage enqueued (rollout excluded) */
+    uint32_t fallbacks;         /* order statistics that took the exact multi-pass path */
+} bmc_stats;
+
+/* Collective hooks for sharded (multi-GPU) statistics.  The stage calls them
+ * at its three merge points with DEVICE buffers, ordered on `stream`
+ * (NCCL on that stream, or torch.distributed with the stream made current).
+ * Partials are exactly mergeable: SUM for counts / limbs / histograms, MIN
+ * for the extrema keys; every rank then finishes with identical bits. */
+enum { BMC_MERGE_SUM = 0, BMC_MERGE_MIN = 1, BMC_MERGE_MAX = 2 };
+typedef struct {
+    void* user;
+    int32_t world;
+    int32_t rank;
+    int (*allreduce_u64)(void* user, uint64_t* buf, size_t count, int op, void* stream);
+    /* recv holds world * count words, rank-ordered */
+    int (*allgather_u64)(void* user, const uint64_t* send, uint64_t* recv, size_t count,
+                         void* stream);
+} bmc_merge;
+
+typedef struct bmc_stats_stage bmc_stats_stage;
+/* A stage sized for up to max_n results per call (candidate capacity). */
+int bmc_stats_create(bmc_ctx* ctx, const bmc_stats_req* req, size_t max_n, bmc_stats_stage** out);
+void bmc_stats_destroy(bmc_stats_stage* st);
+/* Zero the partials (enqueued on stream; NULL = the context's stream). */
+int bmc_stats_begin(bmc_stats_stage* st, void* stream);
+/* Pass 1 over existing device outputs (when no fused rollout fed it). */
+int bmc_stats_accumulate(bmc_stats_stage* st, const double* stop_distance,
+                         const uint8_t* hit_horizon, size_t n, void* stream);
+/* Merge (merge may be NULL: one device), pass 2, selection, read back and
+ * host composition; synchronises the stream. d/hz are this rank's outputs. */
+int bmc_stats_finish(bmc_stats_stage* st, const double* stop_distance, const uint8_t* hit_horizon,
+                     size_t n, const bmc_merge* merge, bmc_stats* out, void* stream);
+/* Rollout with pass 1 fused into its epilogue (st NULL: plain rollout).
+ * Outputs as bmc_cuda_rollout_device; call bmc_stats_begin first. */
+int bmc_cuda_rollout_stats(bmc_ctx* ctx, const bmc_terms* terms, size_t n,
+                           const bmc_world* world, const bmc_run_opts* opts,
+                           const bmc_outputs* out, unsigned long long* total_steps_dev,
+                           bmc_stats_stage* st, void* stream);
+/* One-call convenience over existing device outputs (begin + accumulate + finish). */
+int bmc_cuda_stats(bmc_ctx* ctx, const double* stop_distance, const uint8_t* hit_horizon, size_t n,
+                   const bmc_stats_req* req, bmc_stats* out);
+
+/* Real-time decision with statistics: the graph additionally captures the
+ * fused stage (no merge), so each decision also returns P(collision) per
+ * headway / TTC threshold, min_safe_headway and (optionally) the summary. */
+int bmc_cuda_graph_create_stats(bmc_ctx* ctx, size_t n, const bmc_world* world,
+                                const bmc_run_opts* opts, const bmc_stats_req* req,
+                                bmc_graph** out);
+/* Statistics of the graph's last decision (host composition only). */
+int bmc_cuda_graph_stats(bmc_graph* g, bmc_stats* out);
+
+/* NCCL merge hooks for several devices driven from one process (the C++
+ * MultiCudaRun): ncclCommInitAll over `devices`, one communicator per
+ * device; bmc_nccl_merge(comm) is that rank's bmc_merge (ncclAllReduce /
+ * ncclAllGather of u64 words on the stage's stream).  libnccl.so.2 is opened
+ * at run time (BMC_NCCL_LIB overrides the path); BMC_E_CUDA when absent. */
+typedef struct bmc_comm bmc_comm;
+int bmc_nccl_available(int* version);
+int bmc_nccl_init_all(int ndev, const int* devices, bmc_comm** comms);
+const bmc_merge* bmc_nccl_merge(const bmc_comm* comm);
+void bmc_nccl_destroy(bmc_comm* comm);
+
 /* Device memory for callers without their own CUDA runtime (the C++
  * CudaRun keeps results in HBM through these). */
 int bmc_cuda_alloc(bmc_ctx* ctx, size_t bytes, void** out);

@@ -104,6 +104,30 @@ class Partials(C.Structure):
                 ("any_nan", C.c_int32), ("pad_", C.c_int32)]
 
 
+class StatsReq(C.Structure):
+    _fields_ = [("headways", C.c_void_p), ("n_headways", C.c_size_t), ("risk_levels", C.c_void_p),
+                ("n_risk", C.c_size_t), ("summarize", C.c_int32), ("pad_", C.c_int32),
+                ("bin_width", C.c_double), ("hist_cap", C.c_uint64), ("cand_cap", C.c_uint64)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("horizon_count", C.c_uint64), ("summary", Summary),
+                ("exceed", C.c_void_p), ("min_safe_headway", C.c_void_p),
+                ("histogram", C.c_void_p), ("histogram_cap", C.c_size_t),
+                ("launches", C.c_uint32), ("fallbacks", C.c_uint32)]
+
+
+# bmc_merge: collective hooks of the statistics stage (device buffers, stream-ordered)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+MERGE_SUM, MERGE_MIN, MERGE_MAX = 0, 1, 2
+
+
+class Merge(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("world", C.c_int32), ("rank", C.c_int32),
+                ("allreduce_u64", ALLREDUCE_FN), ("allgather_u64", ALLGATHER_FN)]
+
+
 assert C.sizeof(Sample) == 40 and C.sizeof(Result) == 32 and C.sizeof(Model) == 88
 
 # (name, restype, argtypes) for every entry point declared in brakemc_cuda.h
@@ -165,6 +189,23 @@ SIGNATURES = [
                                      _P]),
     ("bmc_cuda_select_pass", C.c_int, [_P, _P, _P, C.c_size_t, C.c_int, C.c_int, _P,
                                        C.c_size_t, _P]),
+    ("bmc_stats_create", C.c_int, [_P, C.POINTER(StatsReq), C.c_size_t, C.POINTER(_P)]),
+    ("bmc_stats_destroy", None, [_P]),
+    ("bmc_stats_begin", C.c_int, [_P, _P]),
+    ("bmc_stats_accumulate", C.c_int, [_P, _P, _P, C.c_size_t, _P]),
+    ("bmc_stats_finish", C.c_int, [_P, _P, _P, C.c_size_t, C.POINTER(Merge), C.POINTER(Stats),
+                                   _P]),
+    ("bmc_cuda_rollout_stats", C.c_int, [_P, C.POINTER(Terms), C.c_size_t, C.POINTER(World),
+                                         C.POINTER(RunOpts), C.POINTER(Outputs), _P, _P, _P]),
+    ("bmc_cuda_stats", C.c_int, [_P, _P, _P, C.c_size_t, C.POINTER(StatsReq), C.POINTER(Stats)]),
+    ("bmc_cuda_graph_create_stats", C.c_int, [_P, C.c_size_t, C.POINTER(World),
+                                              C.POINTER(RunOpts), C.POINTER(StatsReq),
+                                              C.POINTER(_P)]),
+    ("bmc_cuda_graph_stats", C.c_int, [_P, C.POINTER(Stats)]),
+    ("bmc_nccl_available", C.c_int, [C.POINTER(C.c_int)]),
+    ("bmc_nccl_init_all", C.c_int, [C.c_int, _P, _P]),
+    ("bmc_nccl_merge", C.POINTER(Merge), [_P]),
+    ("bmc_nccl_destroy", None, [_P]),
 ]
 
 _lib = None

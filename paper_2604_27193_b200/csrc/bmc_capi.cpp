@@ -57,75 +57,96 @@ int bucket_count(const WorldDerived& d) {
 
 }  // namespace
 
-int ensure_table(bmc_ctx* ctx, const WorldDerived& d) {
-    if (ctx->have_table && same_key(ctx->tkey, d)) return BMC_OK;
+int ensure_table(bmc_ctx* ctx, const WorldDerived& d, TableEntry** out) {
+    auto& cache = ctx->tables;
+    for (size_t i = 0; i < cache.size(); ++i) {
+        if (same_key(cache[i]->key, d)) {
+            std::rotate(cache.begin(), cache.begin() + static_cast<std::ptrdiff_t>(i),
+                        cache.begin() + static_cast<std::ptrdiff_t>(i) + 1);
+            *out = cache.front().get();
+            return BMC_OK;
+        }
+    }
     const ActuatorTable t = build_actuator_table(d, kTableCap);
-    ctx->have_table = false;
+    auto e = std::make_unique<TableEntry>();
+    e->key = d;
     // The kernel's crossover form of the clamp needs every stage sequence to
     // be non-increasing in n (true whenever brake_cmd < 0 and the RK4 step is
     // stable); anything else runs the generic inline path.
     bool monotone = true;
     double tmin = t.stages.empty() ? 0.0 : t.stages[0].a0;
     for (size_t k = 0; k < t.stages.size(); ++k) {
-        const StageA& e = t.stages[k];
-        for (double vv : {e.a0, e.a1, e.a2, e.a3}) {
+        const StageA& st = t.stages[k];
+        for (double vv : {st.a0, st.a1, st.a2, st.a3}) {
             if (!(vv == vv)) monotone = false;
             tmin = std::min(tmin, vv);
         }
         if (k > 0) {
             const StageA& p = t.stages[k - 1];
-            if (e.a0 > p.a0 || e.a1 > p.a1 || e.a2 > p.a2 || e.a3 > p.a3) monotone = false;
+            if (st.a0 > p.a0 || st.a1 > p.a1 || st.a2 > p.a2 || st.a3 > p.a3) monotone = false;
         }
     }
-    ctx->t_converged = t.converged && monotone;
-    ctx->t_min = tmin;
-    ctx->t_len = static_cast<int>(t.stages.size());
-    ctx->coarse_len = 0;
-    if (ctx->t_converged) {
+    e->converged = t.converged && monotone;
+    e->t_min = tmin;
+    e->t_len = static_cast<int>(t.stages.size());
+    e->coarse_len = 0;
+    if (e->converged) {
+        // fresh buffers, written before any launch can see them
         const size_t bytes = t.stages.size() * sizeof(StageA);
-        BMC_CK(ctx, ctx->d_table.reserve(bytes));
-        BMC_CK(ctx, cudaMemcpy(ctx->d_table.p, t.stages.data(), bytes, cudaMemcpyHostToDevice));
+        BMC_CK(ctx, e->table.reserve(bytes));
+        BMC_CK(ctx, cudaMemcpy(e->table.p, t.stages.data(), bytes, cudaMemcpyHostToDevice));
         // Coarse brake_accel samples for the stop-step predictor: step
         // h = H*dt with H even, a(t) read at t = k*h/2 from the exact table.
         if (d.max_steps > 0 && d.dt > 0.0) {
-            // coarse step ~0.1 s (BMC_COARSE_STEP_S overrides, for tuning):
+            // coarse step ~0.2 s (BMC_COARSE_STEP_S overrides, for tuning):
             // it only orders samples, never changes a result
             double hs = 0.2;
-            if (const char* e = std::getenv("BMC_COARSE_STEP_S")) hs = std::max(1e-6, std::atof(e));
+            if (const char* env = std::getenv("BMC_COARSE_STEP_S")) hs = std::max(1e-6, std::atof(env));
             const long long H = std::max<long long>(2, 2 * std::llround(0.5 * hs / d.dt));
             const long long K = (d.max_steps + H - 1) / H;
             if (K <= kMaxCoarseSteps) {
                 std::vector<float> coarse(static_cast<size_t>(2 * K + 1));
                 for (long long k = 0; k <= 2 * K; ++k) {
-                    const long long idx = std::min<long long>(k * (H / 2), ctx->t_len - 1);
+                    const long long idx = std::min<long long>(k * (H / 2), e->t_len - 1);
                     coarse[static_cast<size_t>(k)] = static_cast<float>(t.stages[idx].a0);
                 }
-                BMC_CK(ctx, ctx->d_coarse.reserve(coarse.size() * sizeof(float)));
-                BMC_CK(ctx, cudaMemcpy(ctx->d_coarse.p, coarse.data(), coarse.size() * sizeof(float),
+                BMC_CK(ctx, e->coarse.reserve(coarse.size() * sizeof(float)));
+                BMC_CK(ctx, cudaMemcpy(e->coarse.p, coarse.data(), coarse.size() * sizeof(float),
                                        cudaMemcpyHostToDevice));
-                ctx->coarse_len = static_cast<int>(coarse.size());
-                ctx->coarse_h = static_cast<float>(static_cast<double>(H) * d.dt);
+                e->coarse_len = static_cast<int>(coarse.size());
+                e->coarse_h = static_cast<float>(static_cast<double>(H) * d.dt);
             }
         }
     }
-    ctx->tkey = d;
-    ctx->have_table = true;
+    if (cache.size() >= kTableCacheEntries) cache.pop_back();  // ~TableEntry: cudaFree waits
+    cache.insert(cache.begin(), std::move(e));
+    *out = cache.front().get();
     return BMC_OK;
+}
+
+ThreadPool& ctx_pool(bmc_ctx* ctx, unsigned threads) {
+    if (!ctx->pool || ctx->pool_threads < threads) {
+        ctx->pool.reset();
+        ctx->pool = std::make_unique<ThreadPool>(threads);
+        ctx->pool_threads = threads;
+    }
+    return *ctx->pool;
 }
 
 int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uint64_t n,
               Plan* plan) {
-    const int rc = ensure_table(ctx, d);
+    TableEntry* te = nullptr;
+    const int rc = ensure_table(ctx, d, &te);
     if (rc != BMC_OK) return rc;
     Plan p;
     p.d = d;
     int mode = opts.table_mode;
-    if (mode == kTableAuto) mode = ctx->t_len <= kSmemTableMax ? kTableShared : kTableGlobal;
-    if (mode == kTableShared && ctx->t_len > kSmemTableMax) mode = kTableGlobal;
-    if (!ctx->t_converged) mode = kTableNone;
+    if (mode == kTableAuto) mode = te->t_len <= kSmemTableMax ? kTableShared : kTableGlobal;
+    if (mode == kTableShared && te->t_len > kSmemTableMax) mode = kTableGlobal;
+    if (!te->converged) mode = kTableNone;
     int sched = opts.schedule;
     if (sched == kScheduleDefault) sched = kScheduleBinned;
-    if (ctx->coarse_len == 0 || mode == kTableNone) sched = kScheduleIndex;
+    if (te->coarse_len == 0 || mode == kTableNone) sched = kScheduleIndex;
     int ilp = opts.ilp != 0 ? opts.ilp : (n >= kIlp2MinSamples ? 2 : 1);
     if (ilp != 1 && ilp != 2) return fail(ctx, BMC_E_CONFIG, "execution.ilp: must be 1 or 2");
     if (mode == kTableNone) ilp = 1;
@@ -135,24 +156,23 @@ int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uin
     int bt = opts.block_threads;
     if (bt == 0) bt = ilp == 2 ? kDefaultIlp2Block : (mode == kTableGlobal ? 256 : 1024);
     const bool ok_bt = ilp == 2 ? (bt == 512 || bt == 640 || bt == 768)
-                                : (bt == 256 || bt == 384 || bt == 512 || bt == 640 ||
-                                   bt == 768 || bt == 1024);
+                                : (bt == 256 || bt == 512 || bt == 768 || bt == 1024);
     if (!ok_bt) {
         return fail(ctx, BMC_E_CONFIG,
                     ilp == 2 ? "execution.block_threads: must be 512, 640 or 768 with ilp 2"
-                             : "execution.block_threads: must be 256, 384, 512, 640, 768 or 1024");
+                             : "execution.block_threads: must be 256, 512, 768 or 1024");
     }
     p.mode = mode;
     p.sched = sched;
     p.bt = bt;
     p.ilp = ilp;
     p.test_block = tb;
-    p.table = ctx->d_table.as<StageA>();
-    p.table_len = ctx->t_len;
-    p.table_min = ctx->t_min;
-    p.coarse = ctx->d_coarse.as<float>();
-    p.coarse_len = ctx->coarse_len;
-    p.coarse_h = ctx->coarse_h;
+    p.table = te->table.as<StageA>();
+    p.table_len = te->t_len;
+    p.table_min = te->t_min;
+    p.coarse = te->coarse.as<float>();
+    p.coarse_len = te->coarse_len;
+    p.coarse_h = te->coarse_h;
     *plan = p;
     return BMC_OK;
 }
@@ -173,7 +193,7 @@ int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n) {
 
 int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms& terms,
                     uint64_t n, const bmc_outputs& out, unsigned long long* total_steps_dev,
-                    cudaStream_t s, KernelEvents* ev, uint32_t* launches) {
+                    cudaStream_t s, KernelEvents* ev, uint32_t* launches, const P1Args* p1) {
     if (n >= (uint64_t{1} << 32)) {
         return fail(ctx, BMC_E_CONFIG, "batch: at most 2^32-1 samples per device launch");
     }
@@ -238,6 +258,7 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
     ra.total_steps = total_steps_dev;
     ra.work_counter = sc.counter.as<unsigned int>();
     ra.counters = reinterpret_cast<unsigned long long*>(sc.counter.as<char>() + 8);
+    if (p1) ra.p1 = *p1;
     if (ev) BMC_CK(ctx, cudaEventRecord(ev->r0, s));
     if (n > 0) {
         BMC_CK(ctx, launch_rollout(ra, plan.mode, plan.bt, plan.ilp, plan.test_block, s));
@@ -317,7 +338,7 @@ namespace {
 int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const bmc_run_opts& o,
                  uint64_t n, const bmc_sample* samples, const bmc_model* model, uint64_t first,
                  bmc_result* host_out, const bmc_outputs* dev_out, bmc_run_info* info,
-                 uint64_t* clamp_count) {
+                 uint64_t* clamp_count, const P1Args* p1 = nullptr) {
     using Clock = std::chrono::steady_clock;
     const uint64_t chunk = std::min<uint64_t>(o.chunk_samples ? o.chunk_samples : default_chunk(n), n);
     const unsigned threads = resolve_threads(o.host_threads);
@@ -368,7 +389,7 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
             const uint8_t* hz = reinterpret_cast<const uint8_t*>(s.h_out.as<char>() + s.len * 12);
             bmc_result* dst = host_out + s.offset;
             const double dt = d.dt;
-            host_pool().parallel_for(
+            ctx_pool(ctx, threads).parallel_for(
                 s.len,
                 [&](size_t b, size_t e) {
                     for (size_t i = b; i < e; ++i) {
@@ -411,7 +432,7 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
             double* hdr = hfl + s.len;
             double* hgr = hdr + s.len;
             std::atomic<int> status{BMC_OK};
-            host_pool().parallel_for(
+            ctx_pool(ctx, threads).parallel_for(
                 s.len,
                 [&](size_t b, size_t e) {
                     int r;
@@ -451,7 +472,7 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
         }
         rc = enqueue_rollout(ctx, plan, s.sc, terms, s.len, outs,
                              ctx->total_steps.as<unsigned long long>(), s.compute, &s.kev,
-                             &launches);
+                             &launches, p1);
         if (rc != BMC_OK) return rc;
         BMC_CK(ctx, cudaEventRecord(s.compute_done, s.compute));
         BMC_CK(ctx, cudaStreamWaitEvent(ctx->d2h, s.compute_done, 0));
@@ -531,7 +552,8 @@ int bmc_cuda_init(int device, bmc_ctx** out) {
         (e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking)) != cudaSuccess ||
-        (e = ctx->kev.create()) != cudaSuccess) {
+        (e = ctx->kev.create()) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->scratch_done, cudaEventDisableTiming)) != cudaSuccess) {
         return fail(nullptr, BMC_E_CUDA, std::string("context setup: ") + cudaGetErrorString(e));
     }
     for (auto& s : ctx->slots) {
@@ -563,7 +585,10 @@ void bmc_cuda_destroy(bmc_ctx* ctx) {
         s.sc.release();
         if (s.compute) cudaStreamDestroy(s.compute);
     }
-    for (bmc::DevBuf* b : {&ctx->d_table, &ctx->d_coarse, &ctx->total_steps, &ctx->draw_ctr, &ctx->partials,
+    ctx->tables.clear();
+    ctx->pool.reset();
+    if (ctx->scratch_done) cudaEventDestroy(ctx->scratch_done);
+    for (bmc::DevBuf* b : {&ctx->total_steps, &ctx->draw_ctr, &ctx->partials,
                            &ctx->sel_hist, &ctx->sel_pref, &ctx->sorted_h, &ctx->buckets,
                            &ctx->hist_buf}) {
         b->release();
@@ -590,21 +615,7 @@ int bmc_cuda_sync(bmc_ctx* ctx) {
 int bmc_cuda_rollout_device(bmc_ctx* ctx, const bmc_terms* terms, size_t n, const bmc_world* world,
                             const bmc_run_opts* opts, const bmc_outputs* out,
                             unsigned long long* total_steps_dev, void* stream) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if (!terms || !world || !out) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_rollout_device: null argument");
-    if (n == 0) return fail(ctx, BMC_E_CONFIG, "batch: must be non-empty");
-    bmc::WorldDerived d{};
-    std::string err;
-    if ((rc = bmc::derive_world(*world, &d, &err)) != BMC_OK) return fail(ctx, rc, err);
-    const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-    bmc::Plan plan;
-    if ((rc = bmc::make_plan(ctx, d, o, n, &plan)) != BMC_OK) return rc;
-    ctx->last_launches = 0;
-    return bmc::enqueue_rollout(ctx, plan, ctx->scratch, *terms, n, *out, total_steps_dev, s,
-                                &ctx->kev, &ctx->last_launches);
+    return bmc_cuda_rollout_stats(ctx, terms, n, world, opts, out, total_steps_dev, nullptr, stream);
 }
 
 int bmc_cuda_last_kernel_ms(bmc_ctx* ctx, float* rollout_ms, float* predict_ms) {

@@ -6,7 +6,9 @@
 #include "bmc_kernels.h"
 #include "bmc_stats.h"
 
+#include <memory>
 #include <string>
+#include <vector>
 
 namespace bmc {
 
@@ -125,6 +127,29 @@ struct Slot {
 
 }  // namespace bmc
 
+namespace bmc {
+
+// The device tables one world needs (actuator stage table, predictor's coarse
+// table).  Entries are immutable once built: a launch in flight always reads
+// the table of its own world, whatever world a later call asks for (a new
+// world gets a new entry; eviction frees, and cudaFree waits for the device).
+struct TableEntry {
+    WorldDerived key{};
+    bool converged = false;
+    double t_min = 0.0;
+    int t_len = 0;
+    DevBuf table, coarse;
+    int coarse_len = 0;
+    float coarse_h = 0.0f;
+    ~TableEntry() {
+        table.release();
+        coarse.release();
+    }
+};
+constexpr size_t kTableCacheEntries = 4;
+
+}  // namespace bmc
+
 struct bmc_ctx {
     int device = 0;
     int sms = 0;
@@ -133,14 +158,19 @@ struct bmc_ctx {
     std::string err;
     std::mutex mu;
 
-    bool have_table = false;
-    bmc::WorldDerived tkey{};
-    bool t_converged = false;
-    double t_min = 0.0;
-    int t_len = 0;
-    bmc::DevBuf d_table, d_coarse;
-    int coarse_len = 0;
-    float coarse_h = 0.0f;
+    // most recently used first
+    std::vector<std::unique_ptr<bmc::TableEntry>> tables;
+
+    // host staging / unpack workers of THIS context (one pool per device,
+    // so several devices driven from one process never queue on each other)
+    std::unique_ptr<bmc::ThreadPool> pool;
+    unsigned pool_threads = 0;
+
+    // the per-context scratch below is reused by every device-resident call;
+    // each launch waits for the previous one's completion event, whatever
+    // stream either was enqueued on
+    cudaEvent_t scratch_done = nullptr;
+    bool scratch_used = false;
 
     bmc::Scratch scratch;
     bmc::DevBuf total_steps;
@@ -177,7 +207,10 @@ inline int prepare(bmc_ctx* ctx) {
 }
 
 // bmc_capi.cpp
-int ensure_table(bmc_ctx* ctx, const WorldDerived& d);
+// The (cached, immutable) table entry of a world.
+int ensure_table(bmc_ctx* ctx, const WorldDerived& d, TableEntry** out);
+// This context's host pool, grown to at least `threads` workers.
+ThreadPool& ctx_pool(bmc_ctx* ctx, unsigned threads);
 int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uint64_t n,
               Plan* plan);
 int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n);
@@ -188,10 +221,35 @@ DrawArgs draw_args(const bmc_model& m, uint64_t first, uint64_t n, const bmc_wor
 // Read back + reset the draw counters; maps flags to BMC_E_DOMAIN/RANGE.
 int finish_draw(bmc_ctx* ctx, const DevBuf& ctr, uint64_t* clamps);
 bool device_sampler_supported(std::string* why);  // bmc_libm_check.cpp
+
+// Statistics stage pieces a CUDA graph captures (bmc_capi_stats.cpp).
+int stats_stage_create(bmc_ctx* ctx, const bmc_stats_req* req, size_t max_n, bmc_stats_stage** out);
+int stats_begin_enqueue(bmc_stats_stage* st, cudaStream_t s);
+// pass-1 words for a rollout; false when the headways are too many to fuse
+bool stats_p1_args(bmc_stats_stage* st, P1Args* p1);
+void fit_stats_plan(Plan* plan, const P1Args& p1);
+// every device stage with no merge (no host read back: capturable)
+int stats_enqueue_device(bmc_stats_stage* st, const double* d, const uint8_t* hz, uint64_t n,
+                         cudaStream_t s);
+// the words the host composition reads, copied into a pinned mirror laid
+// out like the stage memory (stats_mirror_words words)
+size_t stats_mirror_words(const bmc_stats_stage* st);
+int stats_enqueue_readback(bmc_stats_stage* st, uint64_t* mirror, cudaStream_t s);
+int stats_compose_mirror(bmc_stats_stage* st, const uint64_t* mirror, const double* d,
+                         const uint8_t* hz, uint64_t n, bmc_stats* out);
+uint32_t stats_launches(const bmc_stats_stage* st);
 // Enqueue predictor/binning (when planned) + rollout on `s`.  ev may be
 // null (no timing events, e.g. under stream capture).
+// p1 (nullable): fuse statistics pass 1 into the rollout epilogue.
 int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms& terms,
                     uint64_t n, const bmc_outputs& out, unsigned long long* total_steps_dev,
-                    cudaStream_t s, KernelEvents* ev, uint32_t* launches);
+                    cudaStream_t s, KernelEvents* ev, uint32_t* launches,
+                    const P1Args* p1 = nullptr);
+// Legacy statistics calls run on ctx->stream: order them after the last
+// device-resident rollout, whatever stream it was enqueued on.
+inline int order_after_rollouts(bmc_ctx* ctx) {
+    if (ctx->scratch_used) BMC_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->scratch_done, 0));
+    return BMC_OK;
+}
 
 }  // namespace bmc

@@ -35,11 +35,19 @@ struct bmc_graph {
     bmc::DevBuf d_dyn, d_ctr;
     bmc::PinBuf h_dyn, h_ctr;
     uint32_t mlaunches = 0;
+    // Optional statistics stage captured after the rollout (pass 1 fused in
+    // its epilogue); its read-back words land in a pinned mirror per replay.
+    bmc_stats_stage* st = nullptr;
+    bmc::PinBuf h_stats;
+    bool replayed = false;
 };
 
 namespace {
 
 void release(bmc_graph* g) {
+    if (g->st) bmc_stats_destroy(g->st);
+    g->st = nullptr;
+    g->h_stats.release();
     if (g->exec) cudaGraphExecDestroy(g->exec);
     if (g->graph) cudaGraphDestroy(g->graph);
     if (g->mexec) cudaGraphExecDestroy(g->mexec);
@@ -73,12 +81,13 @@ int replay(bmc_graph* g, bmc_result* out, bmc_run_info* info,
     BMC_GK(g, cudaGraphLaunch(model_graph ? g->mexec : g->exec, ctx->stream));
     BMC_GK(g, cudaEventRecord(g->done, ctx->stream));
     BMC_GK(g, cudaEventSynchronize(g->done));
+    g->replayed = true;
     const size_t n = g->n;
     const double* dd = g->h_out.as<double>();
     const int32_t* st = reinterpret_cast<const int32_t*>(g->h_out.as<char>() + n * 8);
     const uint8_t* hz = reinterpret_cast<const uint8_t*>(g->h_out.as<char>() + n * 12);
     const double dt = g->d.dt;
-    bmc::host_pool().parallel_for(
+    bmc::ctx_pool(g->ctx, g->threads).parallel_for(
         n,
         [&](size_t b, size_t e) {
             for (size_t i = b; i < e; ++i) {
@@ -104,6 +113,31 @@ int replay(bmc_graph* g, bmc_result* out, bmc_run_info* info,
         info->total_steps = steps;
     }
     return BMC_OK;
+}
+
+// Inside a capture: the rollout (pass 1 fused when the graph has a stage),
+// the stage's device passes, and the D2H of outputs + statistics words.
+bool capture_rollout_tail(bmc_graph* g, const bmc_terms& terms, const bmc_outputs& outs,
+                          cudaStream_t s, uint32_t* launches) {
+    bmc_ctx* ctx = g->ctx;
+    const size_t n = g->n;
+    bmc::P1Args p1{};
+    if (g->st) {
+        bmc::stats_p1_args(g->st, &p1);
+        if (bmc::stats_begin_enqueue(g->st, s) != BMC_OK) return false;
+    }
+    if (bmc::enqueue_rollout(ctx, g->plan, g->sc, terms, n, outs, g->steps_total.as<unsigned long long>(),
+                             s, nullptr, launches, g->st ? &p1 : nullptr) != BMC_OK) {
+        return false;
+    }
+    if (g->st) {
+        const uint32_t before = bmc::stats_launches(g->st);
+        if (bmc::stats_enqueue_device(g->st, outs.stop_distance, outs.hit_horizon, n, s) != BMC_OK) return false;
+        *launches += bmc::stats_launches(g->st) - before;
+    }
+    if (cudaMemcpyAsync(g->h_out.p, g->d_out.p, n * 13, cudaMemcpyDeviceToHost, s) != cudaSuccess) return false;
+    if (g->st && bmc::stats_enqueue_readback(g->st, g->h_stats.as<uint64_t>(), s) != BMC_OK) return false;
+    return true;
 }
 
 // Capture the device-sampler decision graph (lazily, first model decision).
@@ -136,13 +170,8 @@ int capture_model_graph(bmc_graph* g) {
               cudaMemsetAsync(g->d_ctr.p, 0, 16, s) == cudaSuccess &&
               cudaMemsetAsync(g->steps_total.p, 0, sizeof(unsigned long long), s) == cudaSuccess &&
               bmc::launch_draw_terms(da, ctx->sms, s) == cudaSuccess;
-    if (ok) {
-        ok = bmc::enqueue_rollout(ctx, g->plan, g->sc, terms, n, outs,
-                                  g->steps_total.as<unsigned long long>(), s, nullptr,
-                                  &launches) == BMC_OK;
-    }
-    if (ok) ok = cudaMemcpyAsync(g->h_out.p, g->d_out.p, n * 13, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
-                 cudaMemcpyAsync(g->h_ctr.p, g->d_ctr.p, 16, cudaMemcpyDeviceToHost, s) == cudaSuccess;
+    if (ok) ok = capture_rollout_tail(g, terms, outs, s, &launches);
+    if (ok) ok = cudaMemcpyAsync(g->h_ctr.p, g->d_ctr.p, 16, cudaMemcpyDeviceToHost, s) == cudaSuccess;
     const cudaError_t ec = cudaStreamEndCapture(s, &g->mgraph);
     if (!ok || ec != cudaSuccess) {
         const std::string why = ctx->err.empty() ? cudaGetErrorString(ec) : ctx->err;
@@ -163,8 +192,12 @@ int capture_model_graph(bmc_graph* g) {
 
 extern "C" {
 
-int bmc_cuda_graph_create(bmc_ctx* ctx, size_t n, const bmc_world* world,
-                          const bmc_run_opts* opts, bmc_graph** out) {
+}  // extern "C"
+
+namespace {
+
+int graph_create(bmc_ctx* ctx, size_t n, const bmc_world* world, const bmc_run_opts* opts,
+                 const bmc_stats_req* req, bmc_graph** out) {
     int rc = bmc::prepare(ctx);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -181,6 +214,16 @@ int bmc_cuda_graph_create(bmc_ctx* ctx, size_t n, const bmc_world* world,
     g->threads = bmc::resolve_threads(o.host_threads);
     g->sampler = o.sampler;
     if ((rc = bmc::make_plan(ctx, g->d, o, n, &g->plan)) != BMC_OK) return rc;
+    if (req) {
+        if ((rc = bmc::stats_stage_create(ctx, req, n, &g->st)) != BMC_OK) return rc;
+        bmc::P1Args p1{};
+        if (!bmc::stats_p1_args(g->st, &p1)) {
+            release(g.get());
+            return bmc::fail(ctx, BMC_E_RANGE, "risk.headways: at most 4096 in a decision graph");
+        }
+        bmc::fit_stats_plan(&g->plan, p1);
+        BMC_CK(ctx, g->h_stats.reserve(bmc::stats_mirror_words(g->st) * 8));
+    }
     // private copies of the world-dependent tables
     if (g->plan.table_len > 0 && g->plan.table) {
         const size_t tb = static_cast<size_t>(g->plan.table_len) * sizeof(bmc::StageA);
@@ -213,12 +256,7 @@ int bmc_cuda_graph_create(bmc_ctx* ctx, size_t n, const bmc_world* world,
     uint32_t launches = 0;
     bool ok = cudaMemcpyAsync(g->d_terms.p, g->h_terms.p, n * 32, cudaMemcpyHostToDevice, s) == cudaSuccess &&
               cudaMemsetAsync(g->steps_total.p, 0, sizeof(unsigned long long), s) == cudaSuccess;
-    if (ok) {
-        ok = bmc::enqueue_rollout(ctx, g->plan, g->sc, terms, n, outs,
-                                  g->steps_total.as<unsigned long long>(), s, nullptr,
-                                  &launches) == BMC_OK;
-    }
-    if (ok) ok = cudaMemcpyAsync(g->h_out.p, g->d_out.p, n * 13, cudaMemcpyDeviceToHost, s) == cudaSuccess;
+    if (ok) ok = capture_rollout_tail(g.get(), terms, outs, s, &launches);
     const cudaError_t ec = cudaStreamEndCapture(s, &g->graph);
     if (!ok || ec != cudaSuccess) {
         const std::string why = ctx->err.empty() ? cudaGetErrorString(ec) : ctx->err;
@@ -235,6 +273,36 @@ int bmc_cuda_graph_create(bmc_ctx* ctx, size_t n, const bmc_world* world,
     return BMC_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int bmc_cuda_graph_create(bmc_ctx* ctx, size_t n, const bmc_world* world,
+                          const bmc_run_opts* opts, bmc_graph** out) {
+    return graph_create(ctx, n, world, opts, nullptr, out);
+}
+
+int bmc_cuda_graph_create_stats(bmc_ctx* ctx, size_t n, const bmc_world* world,
+                                const bmc_run_opts* opts, const bmc_stats_req* req,
+                                bmc_graph** out) {
+    if (!req) return bmc::fail(ctx, BMC_E_CONFIG, "bmc_cuda_graph_create_stats: null request");
+    return graph_create(ctx, n, world, opts, req, out);
+}
+
+int bmc_cuda_graph_stats(bmc_graph* g, bmc_stats* out) {
+    if (!g || !out) return bmc::fail(g ? g->ctx : nullptr, BMC_E_CONFIG, "bmc_cuda_graph_stats: null argument");
+    if (!g->st) return bmc::fail(g->ctx, BMC_E_CONFIG, "bmc_cuda_graph_stats: graph has no statistics stage");
+    if (!g->replayed) return bmc::fail(g->ctx, BMC_E_CONFIG, "bmc_cuda_graph_stats: no decision ran yet");
+    int rc = bmc::prepare(g->ctx);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g->ctx->mu);
+    const char* dout = g->d_out.as<char>();
+    rc = bmc::stats_compose_mirror(g->st, g->h_stats.as<uint64_t>(), reinterpret_cast<const double*>(dout),
+                                   reinterpret_cast<const uint8_t*>(dout + g->n * 12), g->n, out);
+    if (rc == BMC_OK) out->launches = g->launches;
+    return rc;
+}
+
 int bmc_cuda_graph_run(bmc_graph* g, const bmc_sample* samples, bmc_result* out,
                        bmc_run_info* info) {
     if (!g || !samples || !out) return bmc::fail(g ? g->ctx : nullptr, BMC_E_CONFIG, "bmc_cuda_graph_run: null argument");
@@ -245,7 +313,7 @@ int bmc_cuda_graph_run(bmc_graph* g, const bmc_sample* samples, bmc_result* out,
     const size_t n = g->n;
     double* h = g->h_terms.as<double>();
     std::atomic<int> status{BMC_OK};
-    bmc::host_pool().parallel_for(
+    bmc::ctx_pool(g->ctx, g->threads).parallel_for(
         n,
         [&](size_t b, size_t e) {
             const int r = bmc::stage_terms_serial(samples + b, e - b, g->world, h + b, h + n + b,
@@ -294,7 +362,7 @@ int bmc_cuda_graph_run_model(bmc_graph* g, const bmc_model* model, uint64_t firs
     double* h = g->h_terms.as<double>();
     std::atomic<int> status{BMC_OK};
     std::atomic<uint64_t> clamps{0};
-    bmc::host_pool().parallel_for(
+    bmc::ctx_pool(g->ctx, g->threads).parallel_for(
         n,
         [&](size_t b, size_t e) {
             uint64_t c = 0;

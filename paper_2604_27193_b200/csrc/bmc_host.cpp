@@ -252,7 +252,15 @@ void ThreadPool::parallel_for(std::size_t n,
 unsigned resolve_threads(int requested) {
     if (requested > 0) return static_cast<unsigned>(requested);
     const unsigned hc = std::thread::hardware_concurrency();
-    return hc ? hc : 1u;
+    // one process per GPU (torchrun sets LOCAL_WORLD_SIZE): share the host's
+    // cores between the local ranks instead of oversubscribing them
+    unsigned local = 1;
+    if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) {
+        const long v = std::strtol(e, nullptr, 10);
+        if (v > 1) local = static_cast<unsigned>(v);
+    }
+    const unsigned t = (hc ? hc : 1u) / local;
+    return t ? t : 1u;
 }
 
 ThreadPool& host_pool() {

@@ -472,9 +472,14 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
         const double2* src = reinterpret_cast<const double2*>(A.table);
         double2* dst = reinterpret_cast<double2*>(smem_raw);
         for (int i = threadIdx.x; i < 2 * len; i += blockDim.x) dst[i] = src[i];
-        __syncthreads();
         tab = reinterpret_cast<const StageA*>(smem_raw);
     }
+    // fused statistics pass 1: per-CTA partials after the table
+    const bool fused = A.p1.sum != nullptr;
+    const P1View sv = p1_view(smem_raw + (MODE == kTableShared ? static_cast<size_t>(len) * sizeof(StageA) : 0),
+                              A.p1.m);
+    if (fused) p1_init(sv, A.p1);
+    if (MODE == kTableShared || fused) __syncthreads();
     const unsigned lane = threadIdx.x & 31u;
     unsigned long long my_steps = 0, my_slots = 0;
     for (;;) {
@@ -493,10 +498,12 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
             if (ok0) {
                 store_out(A, j0, r0);
                 my_steps += static_cast<unsigned>(max(r0.steps, 0));
+                if (fused) p1_add(sv, A.p1.m, r0.x, !r0.stopped);
             }
             if (ok1) {
                 store_out(A, j1, r1);
                 my_steps += static_cast<unsigned>(max(r1.steps, 0));
+                if (fused) p1_add(sv, A.p1.m, r1.x, !r1.stopped);
             }
             const int lmax = max(ok0 ? r0.steps : 0, ok1 ? r1.steps : 0);
             const unsigned gmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(max(lmax, 0)));
@@ -511,6 +518,7 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
             const uint64_t j = A.perm ? static_cast<uint64_t>(A.perm[i]) : i;
             const LaneOut r = MODE == kTableNone ? run_inline(A, j) : run_table<MODE, UNR>(A, tab, len, j, mask);
             store_out(A, j, r);
+            if (fused) p1_add(sv, A.p1.m, r.x, !r.stopped);
             const unsigned st = static_cast<unsigned>(max(r.steps, 0));
             my_steps += st;
             // lane-efficiency bookkeeping: the warp ran max(steps) slots per lane
@@ -519,6 +527,10 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
                 my_slots += static_cast<unsigned long long>(gmax) * __popc(mask);
             }
         }
+    }
+    if (fused) {
+        __syncthreads();
+        p1_flush(sv, A.p1);
     }
     for (int o = 16; o > 0; o >>= 1) {
         my_steps += __shfl_down_sync(0xffffffffu, my_steps, o);
@@ -693,8 +705,9 @@ __global__ void __launch_bounds__(512) fp64_probe_kernel(double* out, int iters,
 template <int MODE, int BT, int ILP, int UNR = 1>
 cudaError_t launch_rollout_t(const RolloutArgs& a, cudaStream_t s) {
     size_t smem = 0;
-    if (MODE == kTableShared) {
-        smem = static_cast<size_t>(a.table_len) * sizeof(StageA);
+    if (MODE == kTableShared) smem = static_cast<size_t>(a.table_len) * sizeof(StageA);
+    if (a.p1.sum) smem += p1_smem_bytes(a.p1.m);
+    if (smem > 0) {
         const cudaError_t e = cudaFuncSetAttribute(rollout_kernel<MODE, BT, ILP, UNR>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    static_cast<int>(smem));
@@ -723,44 +736,43 @@ cudaError_t launch_rollout_t(const RolloutArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Instantiated variants (results never depend on the choice): table modes
+// with one chain per thread at 256/512/768/1024 threads or two chains at
+// 512/640/768, each with the per-step or the blocked termination test; the
+// no-table fallback only with one chain and the per-step test.
+template <int MODE, int ILP, int UNR>
+cudaError_t launch_rollout_b(const RolloutArgs& a, int block_threads, cudaStream_t s) {
+    if constexpr (ILP == 2) {
+        switch (block_threads) {
+            case 512: return launch_rollout_t<MODE, 512, 2, UNR>(a, s);
+            case 640: return launch_rollout_t<MODE, 640, 2, UNR>(a, s);
+            case 768: return launch_rollout_t<MODE, 768, 2, UNR>(a, s);
+            default: return cudaErrorInvalidValue;
+        }
+    } else {
+        switch (block_threads) {
+            case 256: return launch_rollout_t<MODE, 256, 1, UNR>(a, s);
+            case 512: return launch_rollout_t<MODE, 512, 1, UNR>(a, s);
+            case 768: return launch_rollout_t<MODE, 768, 1, UNR>(a, s);
+            case 1024: return launch_rollout_t<MODE, 1024, 1, UNR>(a, s);
+            default: return cudaErrorInvalidValue;
+        }
+    }
+}
+
 template <int MODE>
 cudaError_t launch_rollout_m(const RolloutArgs& a, int block_threads, int ilp, int unroll,
                              cudaStream_t s) {
-    if (unroll == kTestBlock && ilp == 2 && MODE != kTableNone) {
-        switch (block_threads) {
-            case 512: return launch_rollout_t<MODE, 512, 2, kTestBlock>(a, s);
-            case 640: return launch_rollout_t<MODE, 640, 2, kTestBlock>(a, s);
-            case 768: return launch_rollout_t<MODE, 768, 2, kTestBlock>(a, s);
-            default: return cudaErrorInvalidValue;
+    if constexpr (MODE == kTableNone) {
+        return launch_rollout_b<MODE, 1, 1>(a, block_threads, s);
+    } else {
+        const bool blk = unroll == kTestBlock;
+        if (ilp == 2) {
+            return blk ? launch_rollout_b<MODE, 2, kTestBlock>(a, block_threads, s)
+                       : launch_rollout_b<MODE, 2, 1>(a, block_threads, s);
         }
-    }
-    if (unroll == kTestBlock && ilp == 1 && MODE != kTableNone) {
-        switch (block_threads) {
-            case 256: return launch_rollout_t<MODE, 256, 1, kTestBlock>(a, s);
-            case 384: return launch_rollout_t<MODE, 384, 1, kTestBlock>(a, s);
-            case 512: return launch_rollout_t<MODE, 512, 1, kTestBlock>(a, s);
-            case 640: return launch_rollout_t<MODE, 640, 1, kTestBlock>(a, s);
-            case 768: return launch_rollout_t<MODE, 768, 1, kTestBlock>(a, s);
-            case 1024: return launch_rollout_t<MODE, 1024, 1, kTestBlock>(a, s);
-            default: return cudaErrorInvalidValue;
-        }
-    }
-    if (ilp == 2 && MODE != kTableNone) {
-        switch (block_threads) {
-            case 512: return launch_rollout_t<MODE, 512, 2>(a, s);
-            case 640: return launch_rollout_t<MODE, 640, 2>(a, s);
-            case 768: return launch_rollout_t<MODE, 768, 2>(a, s);
-            default: return cudaErrorInvalidValue;
-        }
-    }
-    switch (block_threads) {
-        case 256: return launch_rollout_t<MODE, 256, 1>(a, s);
-        case 384: return launch_rollout_t<MODE, 384, 1>(a, s);
-        case 512: return launch_rollout_t<MODE, 512, 1>(a, s);
-        case 640: return launch_rollout_t<MODE, 640, 1>(a, s);
-        case 768: return launch_rollout_t<MODE, 768, 1>(a, s);
-        case 1024: return launch_rollout_t<MODE, 1024, 1>(a, s);
-        default: return cudaErrorInvalidValue;
+        return blk ? launch_rollout_b<MODE, 1, kTestBlock>(a, block_threads, s)
+                   : launch_rollout_b<MODE, 1, 1>(a, block_threads, s);
     }
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "bmc_internal.h"
+#include "bmc_stats_dev.cuh"
 
 #include <cuda_runtime.h>
 
@@ -46,6 +47,7 @@ struct RolloutArgs {
     unsigned long long* counters;     // nullable: [0] executed steps, [1] lane slots
     const PackedTerms* packed_in;     // nullable: sorted packed inputs (binned schedule)
     PackedOut* packed_out;            // nullable: sorted packed outputs (binned schedule)
+    P1Args p1;                        // fused statistics pass 1 (p1.sum nullptr: off)
 };
 
 struct PredictArgs {

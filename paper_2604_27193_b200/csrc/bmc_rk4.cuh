@@ -1,5 +1,5 @@
 // bmc_rk4.cuh -- the FP64 arithmetic of one RK4 step, shared by every
-// rollout kernel (bmc_kernels.cu, bmc_phase.cu).
+// rollout kernel (bmc_kernels.cu) and the step probe (tools/rk4_step_probe.cu).
 //
 // Every operation is spelled with an explicit _rn intrinsic in the
 // reference's association order (integrator.hpp:39-68, dynamics.hpp:115-132;

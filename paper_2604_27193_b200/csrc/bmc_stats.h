@@ -2,6 +2,8 @@
 #pragma once
 
 #include "bmc_internal.h"
+#include "bmc_stats_core.h"
+#include "bmc_stats_dev.cuh"
 
 #include <cuda_runtime.h>
 
@@ -32,5 +34,21 @@ cudaError_t launch_exceed(const double* d, const uint8_t* hz, uint64_t n, const 
 cudaError_t launch_select(const double* d, const uint8_t* hz, uint64_t n, int exclude_horizon,
                           int shift, const uint64_t* prefixes, int targets,
                           unsigned long long* hist, cudaStream_t s);
+
+
+// fused statistics stage (bmc_fused_stats.cu; orchestration in bmc_stats_pipeline.h)
+cudaError_t launch_pass1(const double* d, const uint8_t* hz, uint64_t n, const P1Args& a, int sms,
+                         cudaStream_t s);
+cudaError_t launch_normalize(const StageDev& g, size_t off, int accs, cudaStream_t s);
+cudaError_t launch_finalize1(const StageDev& g, cudaStream_t s);
+cudaError_t launch_pass2(const double* d, const uint8_t* hz, uint64_t n, const StageDev& g, int sms,
+                         cudaStream_t s);
+cudaError_t launch_targets(const StageDev& g, cudaStream_t s);
+cudaError_t launch_compact(const double* d, const uint8_t* hz, uint64_t n, const StageDev& g,
+                           int sms, cudaStream_t s);
+cudaError_t launch_pack(const StageDev& g, const PackArgs& p, unsigned long long* dst, int sms,
+                        cudaStream_t s);
+cudaError_t launch_select_targets(const StageDev& g, const SelectSegments& seg,
+                                  const unsigned long long* keys, cudaStream_t s);
 
 }  // namespace bmc

@@ -90,6 +90,105 @@ class Collective:
         return np.stack([o.cpu().numpy() for o in out])
 
 
+# ------------------------------------------- merge hooks of the stats stage
+
+_SIGN = -(1 << 63)  # int64 bit pattern 0x8000...: flips unsigned <-> signed order
+
+
+class _CudaWords:
+    """A raw device pointer seen as an int64 tensor (no copy)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class TorchMerge:
+    """bmc_merge over torch.distributed (brakemc_cuda.h): the statistics
+    stage calls these hooks at its merge points with buffers of its own
+    memory -- device pointers for the CUDA engine (NCCL: the collective is
+    enqueued on the stage's stream), host pointers for the host twin used by
+    the gloo tests.  u64 words ride as int64: SUM is the same bits either
+    way; MIN/MAX of unsigned keys run on keys with the sign bit flipped."""
+
+    def __init__(self, dist, device: str = "cuda", world: Optional[int] = None,
+                 rank: Optional[int] = None, via_host: bool = False):
+        from . import _native as N
+        self.N = N
+        self.dist = dist
+        self.device = device
+        # gloo between ranks that hold device buffers: stage through host memory
+        self.via_host = via_host
+        self.world = world if world is not None else dist.get_world_size()
+        self.rank = rank if rank is not None else dist.get_rank()
+        self.error = None
+        self.calls = 0
+        self._ar = N.ALLREDUCE_FN(self._allreduce)
+        self._ag = N.ALLGATHER_FN(self._allgather)
+        self._s = N.Merge(None, self.world, self.rank, self._ar, self._ag)
+
+    def struct(self):
+        return self._s
+
+    def raise_pending(self):
+        if self.error is not None:
+            e, self.error = self.error, None
+            raise e
+
+    def _view(self, ptr, n):
+        import torch
+        if self.device == "cpu":
+            import ctypes
+            arr = np.frombuffer((ctypes.c_int64 * n).from_address(ptr), dtype=np.int64)
+            return torch.from_numpy(arr)
+        return torch.as_tensor(_CudaWords(ptr, n), device=self.device)
+
+    def _stream_ctx(self, stream):
+        import contextlib
+        import torch
+        if self.device == "cpu" or not stream:
+            return contextlib.nullcontext()
+        return torch.cuda.stream(torch.cuda.ExternalStream(stream, device=self.device))
+
+    def _allreduce(self, user, buf, count, op, stream):
+        try:
+            self.calls += 1
+            dev = self._view(buf, count)
+            with self._stream_ctx(stream):
+                t = dev.cpu() if self.via_host else dev
+                if op == self.N.MERGE_SUM:
+                    self.dist.all_reduce(t)
+                else:
+                    t.bitwise_xor_(_SIGN)
+                    self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN if op == self.N.MERGE_MIN
+                                         else self.dist.ReduceOp.MAX)
+                    t.bitwise_xor_(_SIGN)
+                if self.via_host:
+                    dev.copy_(t)
+            return 0
+        except Exception as e:  # noqa: BLE001 -- reported after the C call returns
+            self.error = e
+            return 1
+
+    def _allgather(self, user, send, recv, count, stream):
+        try:
+            self.calls += 1
+            src = self._view(send, count)
+            dst = self._view(recv, count * self.world)
+            with self._stream_ctx(stream):
+                if self.device == "cpu" or self.via_host:
+                    hdst = dst.cpu() if self.via_host else dst
+                    self.dist.all_gather(list(hdst.chunk(self.world)), src.cpu())
+                    if self.via_host:
+                        dst.copy_(hdst)
+                else:
+                    self.dist.all_gather_into_tensor(dst, src)
+            return 0
+        except Exception as e:  # noqa: BLE001
+            self.error = e
+            return 1
+
+
 # ---------------------------------------------------------- dd arithmetic
 
 def dd_merge(a, b):

@@ -261,15 +261,18 @@ class CudaExecutor:
             C.c_void_p(smp.data_ptr()) if smp is not None else None, C.byref(clamps)))
         return t, smp, int(clamps.value)
 
-    def graph(self, n: int, world: SimWorld = SimWorld(), **opts) -> "DecisionGraph":
-        """Capture the real-time decision batch of size n as a CUDA graph."""
-        return DecisionGraph(self, n, world, **opts)
+    def graph(self, n: int, world: SimWorld = SimWorld(), stats=None, **opts) -> "DecisionGraph":
+        """Capture the real-time decision batch of size n as a CUDA graph;
+        ``stats`` (a StatsRequest) adds the fused statistics stage."""
+        return DecisionGraph(self, n, world, stats=stats, **opts)
 
     def rollout_device(self, terms, outputs, world: SimWorld = SimWorld(), total_steps=None,
-                       stream=None, **opts) -> None:
+                       stream=None, stats=None, **opts) -> None:
         """Device-resident rollout. terms: 4 float64 CUDA tensors (v0, floor,
         drag, grade); outputs: (stop_distance f64, steps i32, hit_horizon u8)
-        CUDA tensors or None.  Enqueued on ``stream`` (torch stream or None)."""
+        CUDA tensors or None.  Enqueued on ``stream`` (torch stream or None).
+        ``stats``: a begun StatsStage whose pass 1 is fused into the rollout
+        epilogue (bmc_cuda_rollout_stats)."""
         n = int(terms[0].numel())
         t = N.Terms(*[int(x.data_ptr()) for x in terms])
         o = N.Outputs(*[int(x.data_ptr()) if x is not None else None for x in outputs])
@@ -277,8 +280,24 @@ class CudaExecutor:
         op = self._opts(**opts)
         ts = C.c_void_p(int(total_steps.data_ptr())) if total_steps is not None else None
         st = C.c_void_p(int(stream.cuda_stream)) if stream is not None else None
-        self._check(self.lib.bmc_cuda_rollout_device(self.ctx, C.byref(t), n, C.byref(w),
-                                                     C.byref(op), C.byref(o), ts, st))
+        self._check(self.lib.bmc_cuda_rollout_stats(self.ctx, C.byref(t), n, C.byref(w),
+                                                    C.byref(op), C.byref(o), ts,
+                                                    stats.h if stats is not None else None, st))
+
+    # ------------------------------------------------- fused statistics stage
+    def stats_stage(self, max_n: int, headways=(), risk_levels=(), summarize=False,
+                    bin_width=2.0, hist_cap=0, cand_cap=0):
+        """A device statistics stage (bmc_stats_create) for up to max_n results."""
+        from .stats import StatsRequest, StatsStage
+        return StatsStage(self, StatsRequest(headways, risk_levels, summarize, bin_width, hist_cap,
+                                             cand_cap), max_n)
+
+    def stats(self, d, hz, headways=(), risk_levels=(), summarize=False, bin_width=2.0,
+              hist_cap=0, cand_cap=0) -> dict:
+        """analysis.cpp over device outputs in one call (bmc_cuda_stats)."""
+        from .stats import StatsRequest, stats
+        return stats(self, d, hz, StatsRequest(headways, risk_levels, summarize, bin_width,
+                                               hist_cap, cand_cap))
 
     def last_kernel_ms(self):
         r, p = C.c_float(0), C.c_float(0)
@@ -436,15 +455,30 @@ class CudaExecutor:
 class DecisionGraph:
     """Real-time mode (C2): fixed-size decision batch replayed as a CUDA graph."""
 
-    def __init__(self, ex: CudaExecutor, n: int, world: SimWorld = SimWorld(), **opts):
+    def __init__(self, ex: CudaExecutor, n: int, world: SimWorld = SimWorld(), stats=None,
+                 **opts):
         self.ex = ex
         self.n = n
+        self.req = stats
         w = world.c()
         o = ex._opts(**opts)
         h = C.c_void_p()
-        ex._check(ex.lib.bmc_cuda_graph_create(ex.ctx, n, C.byref(w), C.byref(o), C.byref(h)))
+        if stats is not None:
+            ex._check(ex.lib.bmc_cuda_graph_create_stats(ex.ctx, n, C.byref(w), C.byref(o),
+                                                         C.byref(stats.c()), C.byref(h)))
+        else:
+            ex._check(ex.lib.bmc_cuda_graph_create(ex.ctx, n, C.byref(w), C.byref(o),
+                                                   C.byref(h)))
         self.g = h
         self.out = np.empty(n, dtype=RESULT_DTYPE)
+        if stats is not None:
+            from .stats import StatsOut
+            self._sout = StatsOut(stats)
+
+    def stats(self) -> dict:
+        """Statistics of the last decision (P(collision) per headway, ...)."""
+        self.ex._check(self.ex.lib.bmc_cuda_graph_stats(self.g, C.byref(self._sout.s)))
+        return self._sout.result()
 
     def run(self, samples: np.ndarray) -> RunReport:
         samples = np.ascontiguousarray(samples, dtype=SAMPLE_DTYPE)

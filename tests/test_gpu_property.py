@@ -76,7 +76,7 @@ variants = st.sampled_from([
     dict(ilp=1, block_threads=1024, test_block=8), dict(ilp=1, block_threads=256, test_block=1),
     dict(ilp=2, block_threads=640, test_block=8), dict(ilp=2, block_threads=512, test_block=1),
     dict(ilp=2, block_threads=768, test_block=8, table="global"),
-    dict(ilp=1, block_threads=384, test_block=8, table="global"),
+    dict(ilp=1, block_threads=512, test_block=8, table="global"),
 ])
 
 

@@ -54,7 +54,7 @@ def main():
     if a.quick:
         configs = [c for c in configs if c[0] == "binned" and c[2] >= 512 and c[1] != "none"]
     if a.occupancy:
-        configs = [("binned", t, b, 1, 1) for t in ("shared", "global") for b in (384, 640, 1024)]
+        configs = [("binned", t, b, 1, 1) for t in ("shared", "global") for b in (256, 512, 768, 1024)]
     if a.testblock:
         configs = [("binned", "shared", b, 1, tb) for tb in (1, 8) for b in (768, 1024)]
         configs += [("binned", "shared", b, 2, 8) for b in (512, 640, 768)]
