@@ -667,6 +667,11 @@ def main():
     # a process group whenever launched by torchrun (WORLD_SIZE set), also at
     # N=1, so the scaling run's collective path is the one measured
     if "WORLD_SIZE" in os.environ:
+        if world > 1:
+            # communicator lines ("Init COMPLETE ... nranks N") on stderr, so the
+            # rank count of a scaling run can be read off the log tail
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch
         import torch.distributed as dist
         local_rank = local_rank % max(1, torch.cuda.device_count())

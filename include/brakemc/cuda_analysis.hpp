@@ -11,7 +11,8 @@
 //                                               double-double sums (<= few ulp)
 //   convergence            analysis.cpp:85-124  prefix [0, n_k) reductions
 //   collision_probability  analysis.cpp:145-159 exact count / n
-//   min_safe_headway       analysis.cpp:161-194 exact order statistic
+//   min_safe_headway       analysis.cpp:161-194 exact order statistic (fused
+//                                               statistics stage, bmc_cuda_stats)
 //   build_risk_curve       analysis.cpp:203-228 one O(n log m) pass for the
 //                                               whole grid (reference: O(n m))
 //
@@ -197,21 +198,23 @@ public:
     /// min_safe_headway (analysis.cpp:161-194)
     double min_safe_headway(double risk) const { return min_safe_headways({risk})[0]; }
 
+    /// min_safe_headway per level through the fused statistics stage: one
+    /// level-1 bucket pass, compaction and exact selection (16 levels a call).
     std::vector<double> min_safe_headways(const std::vector<double>& risks) const {
-        std::vector<uint64_t> ranks;
         for (double risk : risks) {
             if (!(risk > 0.0 && risk < 1.0)) {
                 throw ConfigError("risk.level", "must be strictly between 0 and 1");
             }
-            const double raw = (1.0 - risk) * static_cast<double>(n_);
-            ranks.push_back(static_cast<uint64_t>(std::ceil(raw - raw * 1e-12)));
         }
-        std::vector<double> vals(ranks.size());
-        uint64_t stopped = 0;
-        check(bmc_cuda_order_stats(ctx_, dd(), hzp(), n_, 1, ranks.data(), ranks.size(), vals.data(),
-                                   &stopped));
-        for (std::size_t k = 0; k < ranks.size(); ++k) {
-            if (ranks[k] > stopped) vals[k] = std::numeric_limits<double>::infinity();
+        std::vector<double> vals(risks.size());
+        for (std::size_t k0 = 0; k0 < risks.size(); k0 += 16) {
+            const std::size_t m = std::min<std::size_t>(16, risks.size() - k0);
+            bmc_stats_req q{};
+            q.risk_levels = risks.data() + k0;
+            q.n_risk = m;
+            bmc_stats out{};
+            out.min_safe_headway = vals.data() + k0;
+            check(bmc_cuda_stats(ctx_, dd(), hzp(), n_, &q, &out));
         }
         return vals;
     }
@@ -288,16 +291,16 @@ private:
     const double* dd() const { return static_cast<const double*>(d_); }
     const uint8_t* hzp() const { return static_cast<const uint8_t*>(hz_); }
 
-    // prefix_stats (analysis.cpp:85-98): mean / sd (n-1) of the first n
+    // prefix_stats (analysis.cpp:85-98): mean / sd (n-1) of the first n,
+    // with the same exact sums as summarize (so the two agree bit for bit,
+    // like the reference's identical formulas)
     std::pair<double, double> prefix_stats(std::size_t n) const {
-        bmc_partials p{};
-        check(bmc_cuda_partials(ctx_, dd(), hzp(), n, &p));
-        const double mean = (p.sum_hi + p.sum_lo) / static_cast<double>(n);
-        double m[4] = {0, 0, 0, 0};
-        check(bmc_cuda_moments(ctx_, dd(), n, mean, m));
-        const double m2 = m[0] + m[1];
-        const double sd = n > 1 ? std::sqrt(m2 / static_cast<double>(n - 1)) : 0.0;
-        return {mean, sd};
+        bmc_stats_req q{};
+        q.summarize = 1;
+        q.bin_width = 1e300;  // one bin: only the moments are wanted
+        bmc_stats out{};
+        check(bmc_cuda_stats(ctx_, dd(), hzp(), n, &q, &out));
+        return {out.summary.mean, out.summary.sd};
     }
 
     bmc_ctx* ctx_ = nullptr;

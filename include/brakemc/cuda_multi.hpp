@@ -21,6 +21,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -57,11 +58,14 @@ public:
     virtual int allgather_u64(int rank, const std::uint64_t* send, std::uint64_t* recv,
                               std::size_t count, void* stream) = 0;
 
-    /// The bmc_merge the C-ABI stage calls for rank r.
+    /// The bmc_merge the C-ABI stage calls for rank r (callable from every
+    /// rank's thread).
     virtual bmc_merge merge(int rank) {
-        if (hooks_.size() != static_cast<std::size_t>(world())) {
-            hooks_.clear();
-            for (int r = 0; r < world(); ++r) hooks_.push_back(Hook{this, r});
+        {
+            std::lock_guard<std::mutex> lk(hooks_mu_);
+            if (hooks_.empty()) {
+                for (int r = 0; r < world(); ++r) hooks_.push_back(Hook{this, r});
+            }
         }
         bmc_merge m{};
         m.user = &hooks_[static_cast<std::size_t>(rank)];
@@ -83,13 +87,21 @@ private:
         Collective* self;
         int rank;
     };
-    std::vector<Hook> hooks_;
+    std::mutex hooks_mu_;
+    std::vector<Hook> hooks_;  // built once; rank r's hook address is stable
 };
 
 /// NCCL over devices of this process (one communicator per device).
 class NcclCollective : public Collective {
 public:
     explicit NcclCollective(const std::vector<int>& devices) : comms_(devices.size(), nullptr) {
+        for (std::size_t i = 0; i < devices.size(); ++i) {
+            for (std::size_t j = 0; j < i; ++j) {
+                if (devices[i] == devices[j]) {
+                    throw ConfigError("execution.devices", "NCCL needs distinct devices");
+                }
+            }
+        }
         const int rc = bmc_nccl_init_all(static_cast<int>(devices.size()), devices.data(),
                                          comms_.data());
         if (rc != BMC_OK) cuda_detail::raise(rc, bmc_last_error());

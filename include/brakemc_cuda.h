@@ -376,6 +376,12 @@ int bmc_cuda_rollout_stats(bmc_ctx* ctx, const bmc_terms* terms, size_t n,
                            const bmc_world* world, const bmc_run_opts* opts,
                            const bmc_outputs* out, unsigned long long* total_steps_dev,
                            bmc_stats_stage* st, void* stream);
+/* bmc_cuda_run_model with pass 1 fused into every chunk's rollout (the
+ * 1e9-sample stats-only stream); dev_out is required by the later passes. */
+int bmc_cuda_run_model_stats(bmc_ctx* ctx, const bmc_model* model, uint64_t first, size_t n,
+                             const bmc_world* world, const bmc_run_opts* opts, bmc_result* host_out,
+                             const bmc_outputs* dev_out, uint64_t* clamp_count, bmc_run_info* info,
+                             bmc_stats_stage* st);
 /* One-call convenience over existing device outputs (begin + accumulate + finish). */
 int bmc_cuda_stats(bmc_ctx* ctx, const double* stop_distance, const uint8_t* hit_horizon, size_t n,
                    const bmc_stats_req* req, bmc_stats* out);

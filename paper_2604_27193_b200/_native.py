@@ -198,6 +198,10 @@ SIGNATURES = [
     ("bmc_cuda_rollout_stats", C.c_int, [_P, C.POINTER(Terms), C.c_size_t, C.POINTER(World),
                                          C.POINTER(RunOpts), C.POINTER(Outputs), _P, _P, _P]),
     ("bmc_cuda_stats", C.c_int, [_P, _P, _P, C.c_size_t, C.POINTER(StatsReq), C.POINTER(Stats)]),
+    ("bmc_cuda_run_model_stats", C.c_int, [_P, C.POINTER(Model), C.c_uint64, C.c_size_t,
+                                           C.POINTER(World), C.POINTER(RunOpts), _P,
+                                           C.POINTER(Outputs), C.POINTER(C.c_uint64),
+                                           C.POINTER(RunInfo), _P]),
     ("bmc_cuda_graph_create_stats", C.c_int, [_P, C.c_size_t, C.POINTER(World),
                                               C.POINTER(RunOpts), C.POINTER(StatsReq),
                                               C.POINTER(_P)]),

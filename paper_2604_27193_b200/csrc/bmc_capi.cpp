@@ -345,6 +345,7 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
     Plan plan;
     int rc = make_plan(ctx, d, o, chunk, &plan);
     if (rc != BMC_OK) return rc;
+    if (p1) fit_stats_plan(&plan, *p1);
     bool dev_draw = false;
     if (model && (rc = use_device_sampler(ctx, o, &dev_draw)) != BMC_OK) return rc;
     if (dev_draw) {
@@ -585,6 +586,8 @@ void bmc_cuda_destroy(bmc_ctx* ctx) {
         s.sc.release();
         if (s.compute) cudaStreamDestroy(s.compute);
     }
+    if (ctx->stats_cache) bmc_stats_destroy(ctx->stats_cache);
+    ctx->stats_cache = nullptr;
     ctx->tables.clear();
     ctx->pool.reset();
     if (ctx->scratch_done) cudaEventDestroy(ctx->scratch_done);
@@ -770,6 +773,14 @@ int bmc_cuda_run(bmc_ctx* ctx, const bmc_sample* samples, size_t n, const bmc_wo
 int bmc_cuda_run_model(bmc_ctx* ctx, const bmc_model* model, uint64_t first, size_t n,
                        const bmc_world* world, const bmc_run_opts* opts, bmc_result* host_out,
                        const bmc_outputs* dev_out, uint64_t* clamp_count, bmc_run_info* info) {
+    return bmc_cuda_run_model_stats(ctx, model, first, n, world, opts, host_out, dev_out,
+                                    clamp_count, info, nullptr);
+}
+
+int bmc_cuda_run_model_stats(bmc_ctx* ctx, const bmc_model* model, uint64_t first, size_t n,
+                             const bmc_world* world, const bmc_run_opts* opts, bmc_result* host_out,
+                             const bmc_outputs* dev_out, uint64_t* clamp_count, bmc_run_info* info,
+                             bmc_stats_stage* st) {
     int rc = bmc::prepare(ctx);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -782,8 +793,19 @@ int bmc_cuda_run_model(bmc_ctx* ctx, const bmc_model* model, uint64_t first, siz
     std::string err;
     if ((rc = bmc::derive_world(*world, &d, &err)) != BMC_OK) return fail(ctx, rc, err);
     const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
+    bmc::P1Args p1{};
+    if (st) {
+        if (!bmc::stats_p1_args(st, &p1)) {
+            return fail(ctx, BMC_E_RANGE, "risk.headways: at most 4096 when fused into a streamed run");
+        }
+        if (bmc::stats_max_n(st) < n) {
+            return fail(ctx, BMC_E_CONFIG, "stats: more results than the stage was sized for");
+        }
+    }
+    // chunks run on the two slot streams; the stage was begun on ctx->stream,
+    // which run_pipeline synchronises before the first chunk
     return bmc::run_pipeline(ctx, *world, d, o, n, nullptr, model, first, host_out, dev_out, info,
-                             clamp_count);
+                             clamp_count, st ? &p1 : nullptr);
 }
 
 }  // extern "C"

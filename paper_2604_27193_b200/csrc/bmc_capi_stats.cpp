@@ -315,6 +315,12 @@ int stage_finish(bmc_stats_stage* st, const double* d, const uint8_t* hz, uint64
     return BMC_OK;
 }
 
+bool same_config(const StatsConfig& a, const StatsConfig& b) {
+    return a.headways == b.headways && a.order == b.order && a.risks == b.risks &&
+           a.summary == b.summary && a.bin_width == b.bin_width && a.hist_cap == b.hist_cap &&
+           a.cand_cap == b.cand_cap;
+}
+
 int stage_create(bmc_ctx* ctx, const bmc_stats_req* req, size_t max_n, bmc_stats_stage** out) {
     auto st = std::make_unique<bmc_stats_stage>();
     st->ctx = ctx;
@@ -388,6 +394,7 @@ int stats_compose_mirror(bmc_stats_stage* st, const uint64_t* mirror, const doub
     return BMC_OK;
 }
 uint32_t stats_launches(const bmc_stats_stage* st) { return st->launches; }
+size_t stats_max_n(const bmc_stats_stage* st) { return st->max_n; }
 
 }  // namespace bmc
 
@@ -451,13 +458,20 @@ int bmc_cuda_stats(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n,
                                                              : "risk: needs at least one result");
     }
     if (!d) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_stats: null outputs");
-    bmc_stats_stage* st = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(ctx->mu);
-        if ((rc = bmc::stage_create(ctx, req, n, &st)) != BMC_OK) return rc;
-    }
-    std::unique_ptr<bmc_stats_stage, void (*)(bmc_stats_stage*)> guard(st, bmc_stats_destroy);
     std::lock_guard<std::mutex> lk(ctx->mu);
+    // reuse the context's cached stage when the resolved request (and so the
+    // layout and candidate capacity) is the same; the stage's memory is
+    // allocated once per request shape, not per call
+    bmc::StatsConfig cfg;
+    std::string err;
+    if ((rc = bmc::resolve_request(req, n, &cfg, &err)) != BMC_OK) return fail(ctx, rc, err);
+    bmc_stats_stage* st = ctx->stats_cache;
+    if (!st || !bmc::same_config(st->cfg, cfg) || st->max_n < n) {
+        if (st) bmc_stats_destroy(st);
+        ctx->stats_cache = nullptr;
+        if ((rc = bmc::stage_create(ctx, req, n, &st)) != BMC_OK) return rc;
+        ctx->stats_cache = st;
+    }
     cudaStream_t s = ctx->stream;
     if (ctx->scratch_used) BMC_CK(ctx, cudaStreamWaitEvent(s, ctx->scratch_done, 0));
     if ((rc = bmc::stage_begin(st, s)) != BMC_OK) return rc;

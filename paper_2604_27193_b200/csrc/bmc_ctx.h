@@ -177,6 +177,9 @@ struct bmc_ctx {
     bmc::DevBuf draw_ctr;  // device sampler: u64 clamp count + u32 flags
     uint32_t last_launches = 0;
 
+    // the stage bmc_cuda_stats reuses while the request and size class match
+    bmc_stats_stage* stats_cache = nullptr;
+
     bmc::Slot slots[2];
     bmc::DevBuf partials, sel_hist, sel_pref, sorted_h, buckets, hist_buf;
 };
@@ -238,6 +241,7 @@ int stats_enqueue_readback(bmc_stats_stage* st, uint64_t* mirror, cudaStream_t s
 int stats_compose_mirror(bmc_stats_stage* st, const uint64_t* mirror, const double* d,
                          const uint8_t* hz, uint64_t n, bmc_stats* out);
 uint32_t stats_launches(const bmc_stats_stage* st);
+size_t stats_max_n(const bmc_stats_stage* st);
 // Enqueue predictor/binning (when planned) + rollout on `s`.  ev may be
 // null (no timing events, e.g. under stream capture).
 // p1 (nullable): fuse statistics pass 1 into the rollout epilogue.

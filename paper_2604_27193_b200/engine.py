@@ -212,12 +212,13 @@ class CudaExecutor:
 
     def run_model(self, model: UncertaintyModel, n: int, first: int = 0,
                   world: SimWorld = SimWorld(), out: np.ndarray = None, device_out=None,
-                  **opts):
+                  stats=None, **opts):
         """Streaming executor: draw samples [first, first+n) of ``model`` on the
         host pool straight into pinned SoA terms, overlapped with the GPU.
         Results go to a host AoS array (``out``/default) or, when
         ``device_out=(d f64, steps i32, hz u8)`` CUDA tensors are given, stay on
-        the device (stats-only mode).  Returns (RunReport, clamp_count)."""
+        the device (stats-only mode; ``stats``: a begun StatsStage whose pass 1
+        is fused into every chunk's rollout).  Returns (RunReport, clamp_count)."""
         w = world.c()
         o = self._opts(**opts)
         info = N.RunInfo()
@@ -225,9 +226,9 @@ class CudaExecutor:
         m = model.c()
         if device_out is not None:
             outs = N.Outputs(*[int(x.data_ptr()) if x is not None else None for x in device_out])
-            self._check(self.lib.bmc_cuda_run_model(self.ctx, C.byref(m), first, n, C.byref(w),
-                                                    C.byref(o), None, C.byref(outs),
-                                                    C.byref(clamps), C.byref(info)))
+            self._check(self.lib.bmc_cuda_run_model_stats(
+                self.ctx, C.byref(m), first, n, C.byref(w), C.byref(o), None, C.byref(outs),
+                C.byref(clamps), C.byref(info), stats.h if stats is not None else None))
             res = None
         else:
             if out is None:

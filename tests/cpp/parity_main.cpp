@@ -14,6 +14,7 @@
 #include "brakemc/backends.hpp"
 #include "brakemc/cuda_analysis.hpp"
 #include "brakemc/cuda_executor.hpp"
+#include "brakemc/cuda_multi.hpp"
 #include "brakemc/errors.hpp"
 #include "brakemc/sampling.hpp"
 
@@ -222,6 +223,61 @@ int main(int argc, char** argv) {
         const ExecutionReport gpu = run_cuda(b, cfg, geo, phys, o);
         check(verify_consistency(seq, gpu).pass && gpu.worker_count == 3,
               "run_cuda with 3 shards (threads) bit-exact, worker_count = shards");
+    }
+
+    // MultiCudaRun: one context + host thread per device, outputs in HBM, the
+    // whole batch's statistics merged over NCCL (ncclCommInitAll over the
+    // devices; a 1-device communicator on a 1-GPU box) -- every field must
+    // equal the reference's analysis functions (moments: summation bound)
+    {
+        int ndev = 0;
+        bmc_device_count(&ndev);
+        CudaExecOptions o;
+        o.devices.clear();
+        for (int dv = 0; dv < ndev && dv < 8; ++dv) o.devices.push_back(dv);
+        UncertaintyModel m;
+        m.seed = 5;
+        m.friction = NormalSpec{0.45, 0.20};
+        m.grade = NormalSpec{0.0, std::atan(0.06)};
+        const std::size_t n = quick ? 50000 : 300000;
+        const SampleBatch b = draw_batch(m, n);
+        const ExecutionReport ref = run_parallel(b, cfg, geo, phys, 0);
+        int ver = 0;
+        check(bmc_nccl_available(&ver) == BMC_OK, "libnccl opened at run time (version " +
+                                                      std::to_string(ver) + ")");
+        for (bool model_driven : {true, false}) {
+            const MultiCudaRun mr = model_driven ? MultiCudaRun::from_model(m, n, cfg, geo, phys, o)
+                                                 : MultiCudaRun::from_batch(b, cfg, geo, phys, o);
+            ExecutionReport got;
+            got.results = mr.results(cfg.dt);
+            check(verify_consistency(ref, got).pass,
+                  std::string("MultiCudaRun::") + (model_driven ? "from_model" : "from_batch") +
+                      " results bit-exact on " + std::to_string(mr.devices()) + " device(s)");
+            CudaStatsRequest req;
+            req.headways = headway_grid(0.0, 400.0, 2.5);
+            req.risk_levels = {0.5, 0.05, 0.01, 0.001};
+            req.summarize = true;
+            req.bin_width = 0.37;
+            const CudaStats st = mr.statistics(req);  // NCCL merge
+            const DistributionSummary want = summarize(ref.results, 0.37);
+            bool ok = st.n == n && st.horizon_count == want.horizon_count &&
+                      st.summary.min == want.min && st.summary.max == want.max &&
+                      st.summary.median == want.median &&
+                      st.summary.histogram.counts == want.histogram.counts &&
+                      std::abs(st.summary.mean - want.mean) <= 1e-12 * std::abs(want.mean) &&
+                      std::abs(st.summary.sd - want.sd) <= 1e-12 * want.sd;
+            for (std::size_t j = 0; j < req.headways.size(); ++j) {
+                ok = ok && st.collision_probability[j] ==
+                               collision_probability(ref.results, req.headways[j]);
+            }
+            for (std::size_t k = 0; k < req.risk_levels.size(); ++k) {
+                const double w = min_safe_headway(ref.results, req.risk_levels[k]);
+                ok = ok && (st.min_safe_headway[k] == w ||
+                            (std::isinf(w) && std::isinf(st.min_safe_headway[k])));
+            }
+            check(ok, "MultiCudaRun::statistics over NCCL: counts/extrema/median/histogram/"
+                      "collision probabilities/min_safe_headway exact, moments <= 1e-12 rel");
+        }
     }
 
     // run_config.cpp:107-115 / cli.cpp:20-26 with the cuda branch

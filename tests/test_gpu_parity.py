@@ -199,6 +199,19 @@ def test_cpp_executor_api():
     assert p.returncode == 0, p.stdout + p.stderr
 
 
+def test_reference_dispatch_sites_patched_for_cuda():
+    """INTEGRATION.md's edits applied to a copy of the reference's own
+    dispatch sites (tools/integrate_reference.py): config_from_json "cuda",
+    run_configured_executor's body, convergence_table and
+    max_samples_within_budget run the B200 executor; "gpu" still throws."""
+    exe = os.path.join(ROOT, "build", "integration_test")
+    assert os.path.exists(exe), "build/integration_test missing (built by __graft_entry__.build())"
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(p.stdout)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert p.stdout.count("[PASS]") == 5
+
+
 # ------------------------------------------------ streaming / real-time modes
 
 @pytest.mark.parametrize("first,n", [(0, 20000), (123457, 9001)])

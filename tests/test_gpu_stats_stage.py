@@ -227,3 +227,26 @@ def test_two_ranks_on_one_gpu_merge_bitwise(ref):
         outs = [json.load(open(os.path.join(tmp, f"rank{r}.json"))) for r in range(2)]
     for o in outs:
         assert o == _jsonable(single)
+
+
+def test_run_model_stream_with_fused_statistics(ref, executor):
+    """bmc_cuda_run_model_stats: pass 1 in every chunk's rollout (both slot
+    streams), the rest after the stream -- equal to the one-call stage."""
+    import torch
+    m = Model.mixed(19)
+    n = 50001
+    d = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = torch.empty(n, dtype=torch.int32, device="cuda")
+    hz = torch.empty(n, dtype=torch.uint8, device="cuda")
+    samples, _ = ref.draw_batch(m, n)
+    want, _, _ = ref.run(samples, World(), "parallel")
+    req = _request(want)
+    stage = executor.stats_stage(n, req.headways, req.risk_levels, True, 2.0)
+    stage.begin()
+    executor.run_model(bmc.UncertaintyModel(m.seed, *zip(m.mean, m.sd)), n,
+                       device_out=(d, st, hz), stats=stage, chunk=7000)
+    got = stage.finish(d, hz)
+    assert np.array_equal(d.cpu().numpy().view(np.uint64), want["stop_distance"].view(np.uint64))
+    _same(got, host_stats(want["stop_distance"], want["hit_horizon"], req))
+    check_vs_reference(ref, want, got, req)
+    stage.close()

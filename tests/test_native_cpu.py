@@ -107,3 +107,17 @@ def test_no_cpu_fallback_without_device():
         pytest.skip("a CUDA device is present")
     with pytest.raises(bmc.CudaError):
         bmc.CudaExecutor(0)
+
+
+def test_cpp_statistics_merge_fake_collective():
+    """C++ CPU test (tests/cpp/merge_main.cpp): the statistics stage's merge
+    orchestration over brakemc::Collective with an in-process fake, worlds
+    1/2/3, against the reference's analysis functions (built here when the
+    reference tree is present)."""
+    import subprocess
+    exe = os.path.join(ROOT, "build", "merge_cpp")
+    if not os.path.exists(exe):
+        pytest.skip("build/merge_cpp not built (needs the reference headers)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASS" in r.stdout

@@ -38,6 +38,18 @@ import paper_2604_27193_b200 as bmc  # noqa: E402
 from oracle.pyoracle import Model, Reference, World  # noqa: E402
 
 
+
+def noise_seed_for(seed: int) -> int:
+    """Seed of the C4 sensor-noise counter stream: the splitmix64 finaliser of
+    the model seed XOR a domain constant.  (seed + 0x9E3779B97F4A7C15 -- the
+    splitmix64 increment -- would make stream_word(noise_seed, c) equal
+    stream_word(seed, c + 1), i.e. reuse the model's own uniforms.)"""
+    M = (1 << 64) - 1
+    z = (seed ^ 0x5E450C4A0015E5ED) & M
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
 def median_time(fn, reps, warmup=1):
     for _ in range(warmup):
         fn()
@@ -158,7 +170,7 @@ def c4(ref, ex, quick):
     # sensor-noise TTC: trigger at T + eps_i, eps_i ~ N(0, sigma^2) on its own
     # counter stream (the engine's extension; oracle: oracle/bmc_oracle.c)
     from oracle.pyoracle import Port
-    sigma, noise_seed = 0.15, m.seed + 0x9E3779B97F4A7C15
+    sigma, noise_seed = 0.15, noise_seed_for(m.seed)
     t0 = time.perf_counter()
     noisy = ex.exceedance_ttc_noise(d, hz, ttc, v_close, sigma, noise_seed)
     noisy_ms = 1e3 * (time.perf_counter() - t0)

@@ -6,7 +6,9 @@ into pinned SoA chunks streamed H2D on a side stream (--sampler host), while
 the previous chunk rolls out (bmc_cuda_run_model); per-sample outputs stay in
 HBM (13 GB at 1e9) and the
 statistics (summarize, 21-threshold TTC sweep, risk thresholds) run on the
-device.  No AoS batch or per-sample result ever exists on the host.
+device: pass 1 fused into every chunk's rollout, the rest after the stream.
+No AoS batch or per-sample result ever exists on the host.  The statistics
+are recounted with torch's own kernels (integer and order quantities).
 
 python tools/run_1e9.py [--samples 1e9] [--chunk 16777216] [--sampler auto|host|device]
 Prints one JSON line.
@@ -39,27 +41,61 @@ def main():
     st = torch.empty(n, dtype=torch.int32, device="cuda")
     hz = torch.empty(n, dtype=torch.uint8, device="cuda")
     model = bmc.UncertaintyModel(seed=a.seed)
+    ttc = [1.0 + 0.25 * k for k in range(21)]
+    headways = [t * 30.0 for t in ttc]
+    risks = [0.05, 0.01, 0.001, 1e-4, 1e-5]
+    # the statistics stage's pass 1 is fused into every chunk's rollout
+    stage = ex.stats_stage(n, headways, risks, summarize=True, bin_width=2.0)
+    stage.begin()
     t0 = time.perf_counter()
-    rep, clamps = ex.run_model(model, n, device_out=(d, st, hz), chunk=a.chunk, sampler=a.sampler)
+    rep, clamps = ex.run_model(model, n, device_out=(d, st, hz), chunk=a.chunk, sampler=a.sampler,
+                               stats=stage)
     t_roll = time.perf_counter() - t0
     t1 = time.perf_counter()
-    summ = ex.summarize(d, hz, 2.0)
-    ttc = [1.0 + 0.25 * k for k in range(21)]
-    counts = ex.exceedance_counts(d, hz, [t * 30.0 for t in ttc])
-    heads = ex.min_safe_headways(d, hz, [0.05, 0.01, 0.001, 1e-4, 1e-5])
+    out = stage.finish(d, hz)
     t_stats = time.perf_counter() - t1
+    summ = out["summary"]
+    # independent recount with torch's own kernels (integer / order quantities)
+    t2 = time.perf_counter()
+    hb = hz.bool()
+    rec = {"horizon_count": int(hb.sum().item()) == out["horizon_count"],
+           "min": float(d.min().item()) == summ["min"],
+           "max": float(d.max().item()) == summ["max"],
+           "exceedance": all(int((hb | (d > h)).sum().item()) == int(c)
+                             for h, c in zip(headways, out["exceed"]))}
+    k = n // 2 + 1 if n % 2 else None
+    if k is not None:
+        rec["median"] = float(torch.kthvalue(d, k).values.item()) == summ["median"]
+    stopped = d[~hb]
+    ok_msh = True
+    for r, v in zip(risks, out["min_safe_headway"]):
+        raw = (1.0 - r) * float(n)
+        rank = int(math.ceil(raw - raw * 1e-12))
+        w = math.inf if rank > stopped.numel() else float(torch.kthvalue(stopped, rank).values.item())
+        ok_msh = ok_msh and (w == v)
+    rec["min_safe_headway"] = ok_msh
+    del stopped
+    t_rec = time.perf_counter() - t2
     print(json.dumps({
         "samples": n, "seed": a.seed, "chunk": a.chunk, "clamp_count": clamps,
         "sampler": "device" if rep.h2d_bytes == 0 else "host", "h2d_bytes": rep.h2d_bytes,
         "pipeline_s": t_roll, "rollouts_per_s_with_sampling": n / t_roll,
         "rollout_kernel_ms_total": rep.kernel_ms, "kernel_rollouts_per_s": n / (rep.kernel_ms * 1e-3),
         "total_rk4_steps": rep.total_steps, "chunks": rep.chunks,
-        "stats_s": t_stats,
+        "statistics": "pass 1 fused into every chunk's rollout; finish (pass 2, compaction, "
+                      "selection, read back) after the stream",
+        "stats_finish_s": t_stats, "stage_fallbacks": out["fallbacks"],
         "summary": {k: v for k, v in summ.items() if k != "histogram"},
-        "ttc_thresholds_s": ttc, "exceedance_counts": [int(c) for c in counts],
-        "min_safe_headway_m": dict(zip(["0.05", "0.01", "0.001", "1e-4", "1e-5"], heads)),
+        "ttc_thresholds_s": ttc, "exceedance_counts": [int(c) for c in out["exceed"]],
+        "min_safe_headway_m": dict(zip(["0.05", "0.01", "0.001", "1e-4", "1e-5"],
+                                       [float(x) for x in out["min_safe_headway"]])),
+        "recount": {"checks": rec, "all_equal": all(rec.values()),
+                    "how": "torch kernels on the device outputs: sums of (hz | d > h), min/max, "
+                           "kthvalue for the median and min_safe_headway ranks",
+                    "s": t_rec},
         "host_cores": os.cpu_count(),
     }, default=float))
+    stage.close()
 
 
 if __name__ == "__main__":
