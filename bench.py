@@ -76,7 +76,12 @@ def parse():
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi clocks / throttle reasons sampled every period_ms.  Started
+    before the warm-up steps (nvidia-smi's NVML start-up can stall the
+    driver for tens of ms, which must not land in the timed region) and
+    summarised over the rows whose timestamps fall inside the timed window
+    (mark_start / mark_end)."""
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -86,6 +91,8 @@ class ClockSampler:
         self.rows = []
         self.proc = None
         self.thread = None
+        self.t0 = None
+        self.t1 = None
 
     def start(self):
         if self.period_ms <= 0:
@@ -101,11 +108,23 @@ class ClockSampler:
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def _read(self):
+        import datetime
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append(parts)
+            if len(parts) != 8:
+                continue
+            try:
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            self.rows.append((ts, parts[1:]))
 
     def stop(self):
         if self.proc is not None:
@@ -118,7 +137,9 @@ class ClockSampler:
             self.thread.join(timeout=5)
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        for ts, r in self.rows:
+            if ts is not None and self.t0 is not None and not (self.t0 <= ts <= (self.t1 or ts)):
+                continue
             try:
                 sm.append(float(r[0]))
                 mx.append(float(r[1]))
@@ -130,7 +151,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": "timed region only (rows filtered by timestamp)"}
 
 
 # --------------------------------------------------------------- reference
@@ -449,31 +470,42 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     stage = ex.stats_stage(n, headways, risks, summarize=True, bin_width=2.0)
     last = {}
 
+    step_events = []
+
     def step(record=False):
+        # warm-up and timed steps do the same host work (the first call of
+        # anything lazy must not land in the timed region)
         total_steps.zero_()
+        e_a = torch.cuda.Event(enable_timing=True)
+        e_a.record(stream)
         stage.begin()
         ex.rollout_device(dev_terms, (d, st, hz), sw, total_steps=total_steps, stats=stage)
         nl = ex.last_launches()
-        if record:
-            b_ms, r_ms, u_ms = ex.last_stage_ms()
-            kernel_ms.append(r_ms)
-            stage_ms.append((b_ms, u_ms))
+        b_ms, r_ms, u_ms = ex.last_stage_ms()
         h0 = time.perf_counter()
         out = stage.finish(d, hz, merge=merge)
+        h_ms = 1e3 * (time.perf_counter() - h0)
+        e_b = torch.cuda.Event(enable_timing=True)
+        e_b.record(stream)
+        steps_done = int(total_steps.item())
         if record:
+            kernel_ms.append(r_ms)
+            stage_ms.append((b_ms, u_ms))
             launches[0] += nl + out["launches"]
-            stats_host_ms.append(1e3 * (time.perf_counter() - h0))
+            stats_host_ms.append(h_ms)
+            step_events.append((e_a, e_b))
         last["out"] = out
-        return out
+        return steps_done
 
+    clocks = ClockSampler(local_rank, args.clock_ms)
+    clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local_rank, args.clock_ms)
-    clocks.start()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
+    clocks.mark_start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     # the statistics end in a host read back per step: keep the collector
@@ -483,10 +515,10 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     ev0.record(stream)
     steps_sum = 0
     for _ in range(args.steps):
-        step(record=True)
-        steps_sum += int(total_steps.item())
+        steps_sum += step(record=True)
     ev1.record(stream)
     torch.cuda.synchronize()
+    clocks.mark_end()
     gc.enable()
     if dist is not None:
         dist.barrier()
@@ -497,6 +529,10 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
     value = n_total / (ms_per_step * 1e-3)
+    # device span of each timed step and the idle gap before the next one
+    spans = [a.elapsed_time(b) for a, b in step_events]
+    gaps = [step_events[k][1].elapsed_time(step_events[k + 1][0])
+            for k in range(len(step_events) - 1)]
 
     parity = None
     if not args.skip_parity:
@@ -640,7 +676,9 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
             "hbm_streams": hbm_streams,
             "step_breakdown_ms": {"binning": bin_ms, "rollout": roll_ms, "unpermute": unp_ms,
                                   "statistics_wall": sum(stats_host_ms) / len(stats_host_ms),
-                                  "step": ms_per_step},
+                                  "step": ms_per_step,
+                                  "device_span_per_step": spans,
+                                  "gap_between_steps": gaps},
             "e2e": e2e,
             "device_sampler": dsamp,
             "latency_25k": latency,

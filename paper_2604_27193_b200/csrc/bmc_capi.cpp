@@ -177,16 +177,28 @@ int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uin
     return BMC_OK;
 }
 
+// Binned outputs go straight to each sample's index from the rollout
+// epilogue (forward map sorted slot -> sample): the scattered 13-B writes
+// spread over the FP64-bound kernel instead of a separate gather pass.
+// BMC_UNPERMUTE=1 keeps the round-1 packed outputs + unpermute (A/B runs).
+bool unpermute_mode() {
+    static const bool on = [] {
+        const char* e = std::getenv("BMC_UNPERMUTE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n) {
     // counter: [0] work counter (u32) | [8] executed steps | [16] lane slots
     BMC_CK(ctx, sc.counter.reserve(64));
     if (plan.sched == kScheduleBinned) {
         const uint64_t m = std::max<uint64_t>(n, 1);
         BMC_CK(ctx, sc.keys.reserve(m * sizeof(uint16_t)));
-        BMC_CK(ctx, sc.perm.reserve(m * sizeof(uint32_t)));  // inverse permutation
+        BMC_CK(ctx, sc.perm.reserve(m * sizeof(uint32_t)));  // forward (or inverse) permutation
         BMC_CK(ctx, sc.hist.reserve(4096 * sizeof(unsigned int)));
         BMC_CK(ctx, sc.packed_in.reserve(m * sizeof(PackedTerms)));
-        BMC_CK(ctx, sc.packed_out.reserve(m * sizeof(PackedOut)));
+        if (unpermute_mode()) BMC_CK(ctx, sc.packed_out.reserve(m * sizeof(PackedOut)));
     }
     return BMC_OK;
 }
@@ -202,6 +214,8 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
     const WorldDerived& d = plan.d;
     uint32_t nl = 0;
     bool packed = false;
+    const bool any_out = out.stop_distance || out.steps || out.hit_horizon;
+    const bool direct_out = !unpermute_mode();
     if (ev) ev->predicted = false;
     if (plan.sched == kScheduleBinned && n > 0) {
         const int buckets = bucket_count(d);
@@ -228,7 +242,7 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
         BMC_CK(ctx, launch_bin_scatter(sc.keys.as<uint16_t>(), n, sc.hist.as<unsigned int>(),
                                        terms.initial_speed, terms.brake_floor, terms.drag_factor,
                                        terms.grade_accel, sc.packed_in.as<PackedTerms>(),
-                                       sc.perm.as<uint32_t>(), s));
+                                       sc.perm.as<uint32_t>(), direct_out ? 1 : 0, s));
         if (ev) BMC_CK(ctx, cudaEventRecord(ev->p1, s));
         nl += 3;
         packed = true;
@@ -242,7 +256,8 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
     ra.grade = terms.grade_accel;
     ra.perm = nullptr;
     ra.packed_in = packed ? sc.packed_in.as<PackedTerms>() : nullptr;
-    ra.packed_out = packed ? sc.packed_out.as<PackedOut>() : nullptr;
+    ra.packed_out = (packed && !direct_out) ? sc.packed_out.as<PackedOut>() : nullptr;
+    ra.fwd = (packed && direct_out) ? sc.perm.as<uint32_t>() : nullptr;
     ra.n = n;
     ra.dt = d.dt;
     ra.half = d.half;
@@ -266,7 +281,7 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
     }
     if (ev) BMC_CK(ctx, cudaEventRecord(ev->r1, s));
     if (ev) ev->unpermuted = false;
-    if (packed && n > 0 && (out.stop_distance || out.steps || out.hit_horizon)) {
+    if (packed && !direct_out && n > 0 && any_out) {
         BMC_CK(ctx, launch_unpermute(sc.packed_out.as<PackedOut>(), sc.perm.as<uint32_t>(), n,
                                      out.stop_distance, out.steps, out.hit_horizon, s));
         ++nl;

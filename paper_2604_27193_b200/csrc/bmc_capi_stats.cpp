@@ -107,6 +107,7 @@ struct bmc_stats_stage {
     bmc::StatsConfig cfg;
     bmc::StatsLayout L{};
     bmc::DevBuf mem, gather;
+    bmc::PinBuf mirror;  // host copy of the stage words the composition reads
     size_t max_n = 0;
     bool exceed_pending = false;  // headways not accumulated by the last P1 producer
     uint32_t launches = 0;
@@ -227,6 +228,13 @@ struct DeviceBackend {
         if (w == 0) return BMC_OK;
         BMC_CK(ctx(), cudaMemcpyAsync(words(off), host, w * 8, cudaMemcpyHostToDevice, s));
         BMC_CK(ctx(), cudaStreamSynchronize(s));
+        return BMC_OK;
+    }
+    int snapshot(size_t w, const uint64_t** host) {
+        BMC_CK(ctx(), st->mirror.reserve(w * 8));
+        BMC_CK(ctx(), cudaMemcpyAsync(st->mirror.p, st->mem.p, w * 8, cudaMemcpyDeviceToHost, s));
+        BMC_CK(ctx(), cudaStreamSynchronize(s));
+        *host = st->mirror.as<uint64_t>();
         return BMC_OK;
     }
     // exact fallbacks (degenerate data only)
@@ -415,6 +423,7 @@ void bmc_stats_destroy(bmc_stats_stage* st) {
     cudaDeviceSynchronize();
     st->mem.release();
     st->gather.release();
+    st->mirror.release();
     delete st;
 }
 

@@ -38,7 +38,7 @@ struct RegWin {
 };
 
 __device__ __forceinline__ void win_init(RegWin& r) {
-    r.L0 = -1;
+    r.L0 = -1000;  // empty: every first add re-bases
 #pragma unroll
     for (int k = 0; k < kWin; ++k) r.w[k] = 0ull;
 }
@@ -55,17 +55,22 @@ __device__ __forceinline__ void win_flush(RegWin& r, unsigned long long* limbs) 
 
 __device__ __forceinline__ void win_add(RegWin& r, unsigned long long* limbs, int L, uint32_t w0,
                                         uint32_t w1, uint32_t w2) {
+    // a re-based window sits one limb below the value (L0 = L - 1), so the
+    // common offsets are 1 and 0: straight-line adds, no dynamic indexing
     int off = L - r.L0;
-    if (r.L0 < 0 || off < 0 || off > kWin - 3) {
+    if (off != 1 && off != 0) {
         win_flush(r, limbs);
-        r.L0 = min(max(L - 1, 0), sc::kLimbs - kWin);  // room for one smaller and larger limb
+        r.L0 = min(max(L - 1, 0), sc::kLimbs - kWin);
         off = L - r.L0;
     }
-    // predicated adds keep the window in registers (no dynamic indexing)
-#pragma unroll
-    for (int k = 0; k < kWin; ++k) {
-        const unsigned long long a = k == off ? w0 : (k == off + 1 ? w1 : (k == off + 2 ? w2 : 0u));
-        r.w[k] += a;
+    if (off == 1) {
+        r.w[1] += w0;
+        r.w[2] += w1;
+        r.w[3] += w2;
+    } else {
+        r.w[0] += w0;
+        r.w[1] += w1;
+        r.w[2] += w2;
     }
 }
 
@@ -235,6 +240,7 @@ __global__ void __launch_bounds__(kPass2Threads, 2) pass2_kernel(const double* d
     RegAcc m3;
     racc_init(m2);
     racc_init(m3);
+    const double inv_bw = BMC_DIV(1.0, s.bin_width);
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += stride) {
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(kPass2Threads, 2) pass2_kernel(const double* d
         }
         if (sc::is_nan(v)) continue;
         if (hist_on) {
-            const uint64_t idx = sc::hist_index(v, s.lo, s.bin_width, s.bins);
+            const uint64_t idx = sc::hist_index_fast(v, s.lo, s.bin_width, inv_bw, s.bins);
             if (hist_smem) {
                 atomicAdd(&S->hist[idx], 1u);
             } else {
@@ -344,13 +350,18 @@ __global__ void __launch_bounds__(kTargetThreads) targets_kernel(StageDev g) {
     }
 }
 
-// Values in each target's bucket -> that target's candidate list (order keys).
+// Values in each target's bucket -> that target's candidate list (order
+// keys).  A 4096-bit shared bitmap of the target buckets rejects almost
+// every value with one shared load; hit_horizon is read only on a hit.
 __global__ void __launch_bounds__(256) compact_kernel(const double* d, const uint8_t* hz, uint64_t n,
                                                       StageDev g) {
     __shared__ int s_bucket[sc::kMaxTargets];
     __shared__ int s_pop[sc::kMaxTargets];
+    __shared__ unsigned s_map[sc::kB1 / 32];
     __shared__ int s_T;
     const sc::Scalars s = *reinterpret_cast<const sc::Scalars*>(g.w + g.scal);
+    for (int i = threadIdx.x; i < sc::kB1 / 32; i += blockDim.x) s_map[i] = 0u;
+    __syncthreads();
     if (threadIdx.x == 0) {
         const sc::Target* tg = reinterpret_cast<const sc::Target*>(g.w + g.targets);
         int T = 0;
@@ -358,7 +369,10 @@ __global__ void __launch_bounds__(256) compact_kernel(const double* d, const uin
             const bool on = tg[t].valid && tg[t].rank && tg[t].bucket >= 0;
             s_bucket[t] = on ? tg[t].bucket : -1;
             s_pop[t] = tg[t].population;
-            if (on) T = t + 1;
+            if (on) {
+                T = t + 1;
+                s_map[tg[t].bucket >> 5] |= 1u << (tg[t].bucket & 31);
+            }
         }
         s_T = T;
     }
@@ -371,8 +385,8 @@ __global__ void __launch_bounds__(256) compact_kernel(const double* d, const uin
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += stride) {
         const double v = d[i];
-        if (sc::is_nan(v)) continue;
-        const int b = sc::sel_bucket(v, s.sel_lo, s.sel_scale);
+        const int b = sc::sel_bucket(v, s.sel_lo, s.sel_scale);  // NaN -> bucket 0, filtered below
+        if (!((s_map[b >> 5] >> (b & 31)) & 1u) || sc::is_nan(v)) continue;
         const bool h = hz != nullptr && hz[i] != 0;
         for (int t = 0; t < T; ++t) {
             if (s_bucket[t] != b || (s_pop[t] == 1 && h)) continue;
@@ -398,16 +412,37 @@ __global__ void pack_kernel(StageDev g, PackArgs p, unsigned long long* dst) {
 }
 
 // Exact selection of the residual-th smallest candidate key: repeated
-// 12-bit bucketing of [lo, hi] (at most 6 rounds for 64-bit keys, usually 4),
-// each round keeping the bucket that holds the residual rank.
+// 14-bit bucketing of [lo, hi] (a level-1 bucket's keys span ~41 bits, so
+// three rounds), each round keeping the bucket that holds the residual rank.
 constexpr int kSelThreads = 1024;
-constexpr int kSelBins = 4096;
+constexpr int kSelBits = 14;
+constexpr int kSelBins = 1 << kSelBits;
+constexpr int kSelPer = kSelBins / kSelThreads;
+
+template <class F>
+__device__ __forceinline__ void for_keys(const unsigned long long* keys, const SelectSegments& seg,
+                                         int t, uint64_t len, F&& f) {
+    for (int r = 0; r < seg.world; ++r) {
+        const unsigned long long* k = keys + seg.base[t] + static_cast<uint64_t>(r) * seg.rank_stride;
+        uint64_t i = threadIdx.x;
+        // four independent loads in flight per thread (L2-resident keys)
+        for (; i + 3 * kSelThreads < len; i += 4 * kSelThreads) {
+            const unsigned long long a = k[i], b = k[i + kSelThreads], c = k[i + 2 * kSelThreads],
+                                     e = k[i + 3 * kSelThreads];
+            f(a);
+            f(b);
+            f(c);
+            f(e);
+        }
+        for (; i < len; i += kSelThreads) f(k[i]);
+    }
+}
 
 __global__ void __launch_bounds__(kSelThreads) select_kernel(StageDev g, SelectSegments seg,
                                                               const unsigned long long* keys) {
     using Scan = cub::BlockScan<unsigned, kSelThreads>;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ unsigned hist[kSelBins];
+    extern __shared__ __align__(16) unsigned hist[];  // kSelBins
     __shared__ unsigned long long s_lo[32], s_hi[32];
     __shared__ unsigned long long s_bin, s_res;
     const int t = blockIdx.x;
@@ -425,15 +460,11 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(StageDev g, SelectS
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     // min / max key over every rank's segment (pads excluded)
     unsigned long long lo = ~0ull, hi = 0ull;
-    for (int r = 0; r < seg.world; ++r) {
-        const unsigned long long* k = keys + seg.base[t] + static_cast<uint64_t>(r) * seg.rank_stride;
-        for (uint64_t i = threadIdx.x; i < len; i += blockDim.x) {
-            const unsigned long long x = k[i];
-            if (x == ~0ull) continue;
-            lo = x < lo ? x : lo;
-            hi = x > hi ? x : hi;
-        }
-    }
+    for_keys(keys, seg, t, len, [&](unsigned long long x) {
+        if (x == ~0ull) return;
+        lo = x < lo ? x : lo;
+        hi = x > hi ? x : hi;
+    });
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o);
         const unsigned long long b = __shfl_xor_sync(0xffffffffu, hi, o);
@@ -456,22 +487,19 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(StageDev g, SelectS
     while (lo < hi) {
         const unsigned long long span = hi - lo;
         const int nb = 64 - __clzll(static_cast<long long>(span));
-        const int sh = nb > 12 ? nb - 12 : 0;
+        const int sh = nb > kSelBits ? nb - kSelBits : 0;
         for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) hist[i] = 0u;
         __syncthreads();
-        for (int rk = 0; rk < seg.world; ++rk) {
-            const unsigned long long* k = keys + seg.base[t] + static_cast<uint64_t>(rk) * seg.rank_stride;
-            for (uint64_t i = threadIdx.x; i < len; i += blockDim.x) {
-                const unsigned long long x = k[i];
-                if (x < lo || x > hi) continue;  // also drops pads (~0 > hi)
-                atomicAdd(&hist[(x - lo) >> sh], 1u);
-            }
-        }
+        const unsigned long long clo = lo, chi = hi;
+        for_keys(keys, seg, t, len, [&](unsigned long long x) {
+            if (x < clo || x > chi) return;  // also drops pads (~0 > hi)
+            atomicAdd(&hist[(x - clo) >> sh], 1u);
+        });
         __syncthreads();
-        unsigned items[kSelBins / kSelThreads], sum = 0;
+        unsigned items[kSelPer], sum = 0;
 #pragma unroll
-        for (int q = 0; q < kSelBins / kSelThreads; ++q) {
-            items[q] = hist[threadIdx.x * (kSelBins / kSelThreads) + q];
+        for (int q = 0; q < kSelPer; ++q) {
+            items[q] = hist[threadIdx.x * kSelPer + q];
             sum += items[q];
         }
         unsigned excl = 0;
@@ -480,9 +508,9 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(StageDev g, SelectS
         if (excl < r && r <= static_cast<unsigned long long>(excl) + sum) {
             unsigned long long cum = excl;
 #pragma unroll
-            for (int q = 0; q < kSelBins / kSelThreads; ++q) {
+            for (int q = 0; q < kSelPer; ++q) {
                 if (cum + items[q] >= r) {
-                    s_bin = static_cast<unsigned long long>(threadIdx.x * (kSelBins / kSelThreads) + q);
+                    s_bin = static_cast<unsigned long long>(threadIdx.x * kSelPer + q);
                     s_res = r - cum;
                     break;
                 }
@@ -565,7 +593,11 @@ cudaError_t launch_pack(const StageDev& g, const PackArgs& p, unsigned long long
 cudaError_t launch_select_targets(const StageDev& g, const SelectSegments& seg,
                                   const unsigned long long* keys, cudaStream_t s) {
     if (g.n_targets < 1) return cudaSuccess;
-    select_kernel<<<g.n_targets, kSelThreads, 0, s>>>(g, seg, keys);
+    const size_t smem = kSelBins * sizeof(unsigned);
+    const cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    select_kernel<<<g.n_targets, kSelThreads, smem, s>>>(g, seg, keys);
     return cudaGetLastError();
 }
 

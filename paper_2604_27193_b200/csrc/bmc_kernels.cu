@@ -495,13 +495,16 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
             const uint64_t j1 = ok1 ? (A.perm ? static_cast<uint64_t>(A.perm[i1]) : i1) : 0;
             LaneOut r0, r1;
             run_table2<MODE, UNR == kTestBlock>(A, tab, len, j0, j1, ok0, ok1, r0, r1);
+            // outputs at the sample's own index (binned: through the forward map)
+            const uint64_t o0 = (ok0 && A.fwd) ? static_cast<uint64_t>(A.fwd[j0]) : j0;
+            const uint64_t o1 = (ok1 && A.fwd) ? static_cast<uint64_t>(A.fwd[j1]) : j1;
             if (ok0) {
-                store_out(A, j0, r0);
+                store_out(A, o0, r0);
                 my_steps += static_cast<unsigned>(max(r0.steps, 0));
                 if (fused) p1_add(sv, A.p1.m, r0.x, !r0.stopped);
             }
             if (ok1) {
-                store_out(A, j1, r1);
+                store_out(A, o1, r1);
                 my_steps += static_cast<unsigned>(max(r1.steps, 0));
                 if (fused) p1_add(sv, A.p1.m, r1.x, !r1.stopped);
             }
@@ -517,7 +520,7 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
         if (i < A.n) {
             const uint64_t j = A.perm ? static_cast<uint64_t>(A.perm[i]) : i;
             const LaneOut r = MODE == kTableNone ? run_inline(A, j) : run_table<MODE, UNR>(A, tab, len, j, mask);
-            store_out(A, j, r);
+            store_out(A, A.fwd ? static_cast<uint64_t>(A.fwd[j]) : j, r);
             if (fused) p1_add(sv, A.p1.m, r.x, !r.stopped);
             const unsigned st = static_cast<unsigned>(max(r.steps, 0));
             my_steps += st;
@@ -629,7 +632,7 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(const uint16_t* keys, 
                                                           unsigned int* cursor, const double* v0,
                                                           const double* floor_, const double* drag,
                                                           const double* grade, PackedTerms* packed,
-                                                          uint32_t* inv_perm) {
+                                                          uint32_t* perm, int forward) {
     // Tile-aggregated counting-sort scatter: ranks inside a 2048-sample tile
     // come from shared-memory atomics; each (tile, bucket) reserves its slots
     // with ONE global atomic, so hot buckets are not serialised per warp.
@@ -661,7 +664,11 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(const uint16_t* keys, 
             const uint64_t i = tile + static_cast<uint64_t>(k) * 256 + threadIdx.x;
             if (i < n) {
                 const uint32_t pos = s_base[key[k]] + rank[k];
-                inv_perm[i] = pos;
+                if (forward) {
+                    perm[pos] = static_cast<uint32_t>(i);
+                } else {
+                    perm[i] = pos;
+                }
                 // one aligned 32-byte record = one full sector: no read-for-fill
                 double2* dst = reinterpret_cast<double2*>(packed + pos);
                 dst[0] = make_double2(v0[i], floor_[i]);
@@ -829,15 +836,15 @@ cudaError_t launch_bin_scan(unsigned int* hist, int buckets, cudaStream_t s) {
 
 cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* cursor,
                                const double* v0, const double* brake_floor, const double* drag,
-                               const double* grade, PackedTerms* packed, uint32_t* inv_perm,
-                               cudaStream_t s) {
+                               const double* grade, PackedTerms* packed, uint32_t* perm,
+                               int forward, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t blocks_needed = (n + 2047) / 2048;  // one 2048-sample tile per block pass
     const int grid = static_cast<int>(std::min<uint64_t>(blocks_needed,
                                                          static_cast<uint64_t>(sm_count_cached(dev)) * 8));
     bin_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade, packed,
-                                            inv_perm);
+                                            perm, forward);
     return cudaGetLastError();
 }
 

@@ -47,6 +47,8 @@ struct RolloutArgs {
     unsigned long long* counters;     // nullable: [0] executed steps, [1] lane slots
     const PackedTerms* packed_in;     // nullable: sorted packed inputs (binned schedule)
     PackedOut* packed_out;            // nullable: sorted packed outputs (binned schedule)
+    const uint32_t* fwd;              // nullable: sorted slot -> sample index; outputs are then
+                                      // written SoA at the sample's index (no unpermute pass)
     P1Args p1;                        // fused statistics pass 1 (p1.sum nullptr: off)
 };
 
@@ -133,10 +135,12 @@ cudaError_t launch_fp64_probe(double* out, int iters, uint64_t* ops, cudaStream_
 cudaError_t launch_bin_scan(unsigned int* hist_to_cursor, int buckets, cudaStream_t s);
 // counting-sort scatter: inv_perm[i] = sorted slot of sample i, and the
 // sample's inputs are written packed into that slot
+// forward != 0: perm[slot] = i (sorted slot -> sample, for direct SoA
+// outputs); else perm[i] = slot (inverse, for unpermute)
 cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* cursor,
                                const double* v0, const double* brake_floor, const double* drag,
-                               const double* grade, PackedTerms* packed, uint32_t* inv_perm,
-                               cudaStream_t s);
+                               const double* grade, PackedTerms* packed, uint32_t* perm,
+                               int forward, cudaStream_t s);
 // outputs back to index order: out[j] = packed_out[inv_perm[j]]
 cudaError_t launch_unpermute(const PackedOut* packed_out, const uint32_t* inv_perm, uint64_t n,
                              double* stop_distance, int32_t* steps, uint8_t* hit_horizon,

@@ -296,6 +296,27 @@ BMC_HD uint64_t hist_index(double d, double lo, double bw, uint64_t bins) {
     return idx >= bins ? bins - 1 : idx;
 }
 
+// hist_index without the FP64 division on almost every value: the product
+// with the rounded reciprocal is within 1.5 * 2^-52 relative of the exact
+// quotient q = fl((d - lo) / bw), so floor(q) equals floor of the product
+// unless an integer lies within 2^-48 relative of it; those values (and any
+// out-of-range or NaN quotient) take the exact division.  Same bins, bit
+// for bit, as hist_index (tests: tests/test_stats_stage.py edge batches and
+// the device/host-twin comparisons).
+BMC_HD uint64_t hist_index_fast(double d, double lo, double bw, double inv_bw, uint64_t bins) {
+    const double x = BMC_SUB(d, lo);
+    const double qa = BMC_MUL(x, inv_bw);
+    if (qa >= 0.0 && qa < 4503599627370496.0) {  // below 2^52: ulp(qa) < 1
+        const double fa = floor(qa);
+        const double margin = BMC_MUL(qa, 3.552713678800501e-15);  // qa * 2^-48
+        if (BMC_SUB(qa, fa) > margin && BMC_SUB(BMC_ADD(fa, 1.0), qa) > margin) {
+            const uint64_t idx = static_cast<uint64_t>(fa);
+            return idx >= bins ? bins - 1 : idx;
+        }
+    }
+    return hist_index(d, lo, bw, bins);
+}
+
 // Level-1 order-statistic bucket: monotone non-decreasing in d.
 BMC_HD int sel_bucket(double d, double lo, double scale) {
     const double q = BMC_MUL(BMC_SUB(d, lo), scale);

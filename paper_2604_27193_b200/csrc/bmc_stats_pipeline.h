@@ -205,6 +205,7 @@ inline int merge_gather(const bmc_merge* mg, const uint64_t* send, uint64_t* rec
 //   int hist_full(d, n, lo, bw, bins, uint64_t* host_out)   histogram fallback (local)
 //   int select_pass(d, hz, n, exclude, shift, prefixes, m, uint64_t* host_hist)
 //   int read(void* host, size_t offset, size_t words)   synchronising copy
+//   int snapshot(size_t words, const uint64_t** host)   stage words [0, words) on the host
 //   int write(size_t offset, const void* host, size_t words)
 //
 // Part 1: every device stage up to the selected order statistics.  With no
@@ -453,8 +454,17 @@ int stats_finish(B& be, const StatsConfig& cfg, const StatsLayout& L, const doub
                  void* stream, uint32_t* launches, std::string* err) {
     int rc = stats_device_stages(be, cfg, L, d, hz, n, mg, stream, err);
     if (rc != BMC_OK) return rc;
+    // one synchronising copy of the stage words [0, L.cand) (~140 KB), then
+    // the composition reads host memory
+    const uint64_t* snap = nullptr;
+    if ((rc = be.snapshot(L.cand, &snap)) != BMC_OK) return rc;
     StatsReadback rb;
-    rc = stats_read([&](void* h, size_t off, size_t w) { return be.read(h, off, w); }, cfg, L, &rb);
+    rc = stats_read(
+        [&](void* h, size_t off, size_t w) {
+            std::memcpy(h, snap + off, w * 8);
+            return BMC_OK;
+        },
+        cfg, L, &rb);
     if (rc != BMC_OK) return rc;
     rc = stats_compose(be, cfg, L, rb, d, hz, n, mg, out, stream, err);
     if (launches) *launches = 0;

@@ -1,5 +1,18 @@
 """Sharded statistics: one process per GPU, contiguous index shards.
 
+Product path: ``TorchMerge`` -- the bmc_merge hooks of the fused statistics
+stage (stats.StatsStage.finish(..., merge=TorchMerge(dist))) over
+torch.distributed: three merge points per step (P1 partials SUM + extrema
+MIN, P2 partials SUM, candidate counts + keys all-gather), every collective
+on device buffers in the stage's stream (NCCL), and exact partials (integer
+counts, u64 limbs of exact sums), so every rank finishes with the
+single-device answer bit for bit.  bench.py uses it under torchrun.
+
+The quantity-by-quantity merge below (Collective / HostShard / DeviceShard:
+one small collective per quantity, radix select with one allreduce per
+8-bit pass) is the round-1 path, kept for callers that want one statistic
+and as a second, independent implementation the tests cross-check.
+
 SURVEY.md section 8(e): sample i depends only on (seed, i) (sampling.hpp:3-6),
 so rank r owns [r*N/G, (r+1)*N/G) and nothing crosses devices on the data
 path.  The statistics of analysis.cpp combine with one small allreduce per

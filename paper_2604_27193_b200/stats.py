@@ -97,7 +97,10 @@ class StatsStage:
             int(d.numel()), st))
 
     def finish(self, d, hz, merge=None, stream=None, hist_cap: int = 1 << 16) -> dict:
-        out = StatsOut(self.req, hist_cap)
+        # result arrays allocated once per stage (a bench step calls this every step)
+        out = self._out if getattr(self, "_out", None) is not None and \
+            self._out.hist.size == max(1, hist_cap) else StatsOut(self.req, hist_cap)
+        self._out = out
         st = C.c_void_p(int(stream.cuda_stream)) if stream is not None else None
         mg = C.byref(merge.struct()) if merge is not None else None
         n = int(d.numel()) if d is not None else 0

@@ -189,6 +189,11 @@ struct HostBackend {
         std::memcpy(words(off), host, w * 8);
         return BMC_OK;
     }
+    int snapshot(size_t w, const uint64_t** host) {
+        (void)w;
+        *host = st->mem.data();
+        return BMC_OK;
+    }
     int hist_full(const double* d, uint64_t n, double lo, double bw, uint64_t bins, uint64_t* out) {
         for (uint64_t i = 0; i < n; ++i) {
             if (!sc::is_nan(d[i])) out[sc::hist_index(d[i], lo, bw, bins)] += 1;
@@ -254,6 +259,19 @@ int bmch_stats_run(const double* d, const uint8_t* hz, size_t n, const bmc_stats
     }
     if (rc != BMC_OK && err && errcap) std::snprintf(err, errcap, "%s", e.c_str());
     return rc;
+}
+
+// hist_index_fast (the kernels' division-free path) against the exact
+// hist_index on caller-chosen values; returns the number of disagreements.
+uint64_t bmch_hist_index_mismatches(const double* v, size_t n, double lo, double bw,
+                                    uint64_t bins) {
+    using namespace bmc;
+    const double inv = 1.0 / bw;
+    uint64_t bad = 0;
+    for (size_t i = 0; i < n; ++i) {
+        if (sc::hist_index_fast(v[i], lo, bw, inv, bins) != sc::hist_index(v[i], lo, bw, bins)) ++bad;
+    }
+    return bad;
 }
 
 // The exact sum of the stage's arithmetic, for unit tests of the

@@ -30,6 +30,9 @@ def lib():
                                      C.c_char_p, C.c_size_t]
         L.bmch_exact_sum.restype = C.c_double
         L.bmch_exact_sum.argtypes = [C.c_void_p, C.c_size_t]
+        L.bmch_hist_index_mismatches.restype = C.c_uint64
+        L.bmch_hist_index_mismatches.argtypes = [C.c_void_p, C.c_size_t, C.c_double, C.c_double,
+                                                 C.c_uint64]
         _lib = L
     return _lib
 
@@ -56,3 +59,8 @@ def host_stats(d, hz, req: StatsRequest, merge=None, cand_cap: int = 0, hist_cap
         exc.code = rc
         raise exc
     return out.result()
+
+
+def hist_index_mismatches(v, lo, bw, bins) -> int:
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    return int(lib().bmch_hist_index_mismatches(C.c_void_p(v.ctypes.data), v.size, lo, bw, bins))

@@ -187,7 +187,9 @@ def test_device_resident_path(ref, executor):
     assert int(total.item()) == int(want["steps"].sum())
     rms, pms = executor.last_kernel_ms()
     assert rms > 0.0
-    assert executor.last_launches() == 5  # predict, scan, scatter, rollout, unpermute
+    # predict, scan, scatter, rollout (outputs written at each sample's index
+    # through the forward map: no unpermute pass unless BMC_UNPERMUTE=1)
+    assert executor.last_launches() == (5 if os.environ.get("BMC_UNPERMUTE") == "1" else 4)
 
 
 def test_cpp_executor_api():

@@ -142,3 +142,23 @@ def test_sensor_noise_ttc_shards_add_up(executor, mixed):
     b = executor.exceedance_ttc_noise(d[cut:], hz[cut:], TTC[::-1], 30.0, 0.2, noise_seed=11,
                                       first=cut)
     assert (a + b).tolist() == whole.tolist()
+
+
+@pytest.mark.parametrize("sigma", [0.05, 0.3])
+def test_sensor_noise_sweep_on_the_reference_normal_stream(ref, executor, mixed, sigma):
+    # pins the noisy sweep to the REFERENCE itself, not only the C oracle:
+    # eps_i = sigma * standard_normal_at(noise_seed, first + i) from the
+    # unmodified reference (sampling.cpp:48-53 via oracle/_ref), then the
+    # collision rule d > (T + eps_i) * v (IEEE, in the kernel's op order) and
+    # horizon hits always colliding (analysis.cpp:152-157)
+    n = 20000
+    res = mixed[:n]
+    first, seed, v = 4321, 0x5EED, 30.0
+    z = np.array([ref.standard_normal_at(seed, first + i) for i in range(n)])
+    eps = sigma * z
+    d_host = res["stop_distance"]
+    hz_host = res["hit_horizon"] != 0
+    want = [int(np.count_nonzero(hz_host | (d_host > (t + eps) * v))) for t in TTC]
+    d, hz = device(res)
+    got = executor.exceedance_ttc_noise(d, hz, TTC, v, sigma, noise_seed=seed, first=first)
+    assert got.tolist() == want

@@ -24,7 +24,7 @@ from oracle.pyoracle import Model, World
 from paper_2604_27193_b200.stats import StatsRequest
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-from hoststats import exact_sum, host_stats  # noqa: E402
+from hoststats import exact_sum, hist_index_mismatches, host_stats  # noqa: E402
 
 RISKS = [0.05, 0.01, 0.001, 0.5]
 EPS = 2.0 ** -52
@@ -103,6 +103,20 @@ def test_exact_sum_is_order_independent():
     for _ in range(3):
         rng.shuffle(v)
         assert exact_sum(v) == s
+
+
+@pytest.mark.parametrize("lo,bw", [(20.0, 2.0), (20.0, 0.37), (-5.0, 0.1), (0.0, 1e-3),
+                                   (37.0, 3.0), (1e6, 0.7)])
+def test_division_free_histogram_index_is_exact(lo, bw):
+    # the kernels' hist_index_fast must equal (size_t)((d - lo) / bw) on every
+    # value, above all on the bin edges lo + k*bw and their neighbours
+    rng = np.random.default_rng(3)
+    k = np.arange(0, 5000, dtype=np.float64)
+    edges = lo + k * bw
+    v = np.concatenate([edges, np.nextafter(edges, np.inf), np.nextafter(edges, -np.inf),
+                        lo + (k + 0.5) * bw, lo + rng.uniform(0, 5000 * bw, 200000),
+                        [lo, np.nextafter(lo, np.inf), lo + 1e-300]])
+    assert hist_index_mismatches(v, lo, bw, 4000) == 0
 
 
 # ----------------------------------------------------- single rank vs ref
