@@ -540,14 +540,21 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
                                    cdev, headways, risks)
     stats_out = last["out"]
     roll_ms = sum(kernel_ms) / len(kernel_ms)
-    traffic, traffic_detail = None, None
-    tpath = os.path.join(ROOT, "profiles", "rollout_traffic.json")
+    # DRAM traffic per kernel from the ncu --set full capture of this same
+    # step at 1e8 (tools/profile_headline.py -> tools/ncu_traffic.py); the
+    # capture's per-sample bytes scale to this launch when n differs
+    traffic, traffic_detail, ncu_k = None, None, {}
+    tpath = os.path.join(ROOT, "profiles", "round2_traffic.json")
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
-        traffic = tj["bytes_per_sample"] * n  # DRAM bytes per launch (ncu), this launch's n
-        traffic_detail = {"bytes_per_sample": tj["bytes_per_sample"],
-                          "algorithmic_bytes_per_sample": tj["algorithmic_bytes_per_sample"],
-                          "source": tj["source"] + ", scaled to this launch's sample count"}
+        ncu_k = tj["kernels"]
+        if "rollout_kernel" in ncu_k:
+            bps = ncu_k["rollout_kernel"]["bytes_per_sample"]
+            traffic = bps * n
+            traffic_detail = {"bytes_per_sample": bps, "algorithmic_bytes_per_sample": 48,
+                              "source": tj["source"] + (
+                                  "" if int(tj["samples"]) == n else
+                                  ", scaled from %d samples to this launch's" % int(tj["samples"]))}
     steps_per_launch = steps_sum / args.steps
     hbm_peak, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
     ppath = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -556,19 +563,33 @@ def b200_arm(args, rank, world, local_rank, dist, coll_device=None):
     bin_ms = sum(b for b, _ in stage_ms) / len(stage_ms)
     unp_ms = sum(u for _, u in stage_ms) / len(stage_ms)
 
-    def stream(bytes_per_sample, ms, what):
+    def stream(bytes_per_sample, ms, what, kernels):
         gbs = bytes_per_sample * n / (ms * 1e-3) / 1e9 if ms > 0 else None
-        return {"what": what, "bytes_per_sample": bytes_per_sample, "ms": ms, "gb_per_s": gbs,
-                "frac_of_hbm_peak": gbs / hbm_peak if gbs else None}
+        dram = [ncu_k[k]["bytes_per_sample"] for k in kernels if k in ncu_k]
+        return {"what": what, "algorithmic_bytes_per_sample": bytes_per_sample, "ms": ms,
+                "gb_per_s": gbs, "frac_of_hbm_peak": gbs / hbm_peak if gbs else None,
+                "dram_bytes_per_sample_ncu": sum(dram) if len(dram) == len(kernels) else None}
 
     hbm_streams = {
         "peak_gb_per_s": hbm_peak, "peak_source": hbm_src,
         "sample_stream": stream(SAMPLE_STREAM_BYTES, bin_ms,
-                                "predict + binning scatter: terms in, packed sorted records out"),
-        "rollout": stream(traffic / n if traffic else 48.0, roll_ms,
-                          "rollout kernel DRAM bytes (ncu) over its time -- FP64-bound"),
+                                "predict + binning scatter: terms in, packed sorted records out",
+                                ["predict_kernel", "bin_scatter_kernel"]),
+        "rollout": stream(48.0, roll_ms,
+                          "rollout kernel: packed records in, packed outputs out -- FP64-bound",
+                          ["rollout_kernel"]),
         "result_stream": stream(RESULT_STREAM_BYTES, unp_ms,
-                                "unpermute: packed sorted outputs -> index-order outputs"),
+                                "unpermute: packed sorted outputs -> index-order outputs",
+                                ["unpermute_kernel"]),
+        "statistics_passes": {"what": "pass 2 (d + hit_horizon) and compaction (d, hit_horizon "
+                                      "on a hit): 18 algorithmic B/sample",
+                              "dram_bytes_per_sample_ncu": (
+                                  ncu_k["pass2_kernel"]["bytes_per_sample"] +
+                                  ncu_k["compact_kernel"]["bytes_per_sample"])
+                              if "pass2_kernel" in ncu_k and "compact_kernel" in ncu_k else None,
+                              "ms_ncu": (ncu_k["pass2_kernel"]["time_ms"] +
+                                         ncu_k["compact_kernel"]["time_ms"])
+                              if "pass2_kernel" in ncu_k and "compact_kernel" in ncu_k else None},
     }
     achieved = ALGO_FLOPS_PER_STEP * steps_per_launch / (roll_ms * 1e-3)
     executed = EXEC_FLOPS_PER_STEP * steps_per_launch / (roll_ms * 1e-3)

@@ -177,14 +177,18 @@ int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uin
     return BMC_OK;
 }
 
-// Binned outputs go straight to each sample's index from the rollout
-// epilogue (forward map sorted slot -> sample): the scattered 13-B writes
-// spread over the FP64-bound kernel instead of a separate gather pass.
-// BMC_UNPERMUTE=1 keeps the round-1 packed outputs + unpermute (A/B runs).
+// Binned outputs: the rollout writes packed 16-B records in sorted order
+// (full sectors, coalesced) and unpermute gathers them into index order --
+// measured at 1e8: rollout DRAM traffic 45.8 B/sample + unpermute 73
+// B/sample, 942.6 ms/step.  BMC_DIRECT_OUTPUTS=1 instead writes each
+// sample's outputs at its own index from the rollout epilogue through a
+// forward map (no unpermute pass; 940.6 ms/step, but the scattered partial
+// writes cost 226 B/sample of read-modify-write traffic inside the rollout,
+// hidden under its FP64 bound).  profiles/round2_summary.md has both.
 bool unpermute_mode() {
     static const bool on = [] {
-        const char* e = std::getenv("BMC_UNPERMUTE");
-        return e && e[0] == '1';
+        const char* e = std::getenv("BMC_DIRECT_OUTPUTS");
+        return !(e && e[0] == '1');
     }();
     return on;
 }

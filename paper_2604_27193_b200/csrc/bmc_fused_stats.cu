@@ -217,8 +217,9 @@ struct P2Smem {
 // dev*dev and (dev*dev)*dev rounded as written), the summarize histogram
 // (:64-75) and the level-1 order-statistic histograms (all / stoppers).
 constexpr int kPass2Threads = 512;
+constexpr int kUnroll = 4;
 
-__global__ void __launch_bounds__(kPass2Threads, 2) pass2_kernel(const double* d, const uint8_t* hz,
+__global__ void __launch_bounds__(kPass2Threads, 1) pass2_kernel(const double* d, const uint8_t* hz,
                                                                  uint64_t n, StageDev g) {
     extern __shared__ __align__(16) unsigned char sm[];
     P2Smem* S = reinterpret_cast<P2Smem*>(sm);
@@ -241,18 +242,14 @@ __global__ void __launch_bounds__(kPass2Threads, 2) pass2_kernel(const double* d
     racc_init(m2);
     racc_init(m3);
     const double inv_bw = BMC_DIV(1.0, s.bin_width);
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += stride) {
-        const double v = d[i];
-        const bool h = hz != nullptr && hz[i] != 0;
+    auto one = [&](double v, bool h) {
         if (summary) {
             const double dev = BMC_SUB(v, s.mean);
             const double sq = BMC_MUL(dev, dev);
             racc_add(m2, S->acc, sq);
             racc_add(m3, S->acc + sc::kAccWords, BMC_MUL(sq, dev));
         }
-        if (sc::is_nan(v)) continue;
+        if (sc::is_nan(v)) return;
         if (hist_on) {
             const uint64_t idx = sc::hist_index_fast(v, s.lo, s.bin_width, inv_bw, s.bins);
             if (hist_smem) {
@@ -264,7 +261,23 @@ __global__ void __launch_bounds__(kPass2Threads, 2) pass2_kernel(const double* d
         const int b = sc::sel_bucket(v, s.sel_lo, s.sel_scale);
         atomicAdd(&S->sel_all[b], 1u);
         if (!h) atomicAdd(&S->sel_stop[b], 1u);
+    };
+    // kUnroll independent loads in flight per thread (the pass is latency-
+    // bound on its streaming reads, not on arithmetic)
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+        double v[kUnroll];
+        uint8_t h[kUnroll];
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) {
+            v[k] = __ldcs(d + i + k * stride);
+            h[k] = hz != nullptr ? __ldcs(hz + i + k * stride) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) one(v[k], h[k] != 0);
     }
+    for (; i < n; i += stride) one(d[i], hz != nullptr && hz[i] != 0);
     racc_flush(m2, S->acc);
     racc_flush(m3, S->acc + sc::kAccWords);
     __syncthreads();
@@ -381,19 +394,26 @@ __global__ void __launch_bounds__(256) compact_kernel(const double* d, const uin
     if (T == 0) return;
     unsigned long long* cnt = g.w + g.cand_count;
     unsigned long long* cand = g.w + g.cand;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += stride) {
-        const double v = d[i];
+    auto one = [&](uint64_t i, double v) {
         const int b = sc::sel_bucket(v, s.sel_lo, s.sel_scale);  // NaN -> bucket 0, filtered below
-        if (!((s_map[b >> 5] >> (b & 31)) & 1u) || sc::is_nan(v)) continue;
+        if (!((s_map[b >> 5] >> (b & 31)) & 1u) || sc::is_nan(v)) return;
         const bool h = hz != nullptr && hz[i] != 0;
         for (int t = 0; t < T; ++t) {
             if (s_bucket[t] != b || (s_pop[t] == 1 && h)) continue;
             const unsigned long long pos = atomicAdd(&cnt[t], 1ull);
             if (pos < g.cand_cap) cand[static_cast<uint64_t>(t) * g.cand_cap + pos] = sc::order_key(v);
         }
+    };
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+        double v[kUnroll];
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) v[k] = __ldcs(d + i + k * stride);
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) one(i + k * stride, v[k]);
     }
+    for (; i < n; i += stride) one(i, d[i]);
 }
 
 // Local candidates -> one padded block [t0: P0][t1: P1]... (UINT64_MAX pads).
@@ -567,7 +587,7 @@ cudaError_t launch_pass2(const double* d, const uint8_t* hz, uint64_t n, const S
     cudaError_t e = cudaFuncSetAttribute(pass2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    pass2_kernel<<<grid_for(n, sms, 2, kPass2Threads), kPass2Threads, smem, s>>>(d, hz, n, g);
+    pass2_kernel<<<grid_for(n, sms, 1, kPass2Threads), kPass2Threads, smem, s>>>(d, hz, n, g);
     return cudaGetLastError();
 }
 

@@ -29,6 +29,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include <climits>
+#include <cstdlib>
 
 namespace bmc {
 namespace {
@@ -628,6 +629,7 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(unsigned int* hist, int 
     }
 }
 
+template <int kItems>
 __global__ void __launch_bounds__(256) bin_scatter_kernel(const uint16_t* keys, uint64_t n,
                                                           unsigned int* cursor, const double* v0,
                                                           const double* floor_, const double* drag,
@@ -636,7 +638,6 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(const uint16_t* keys, 
     // Tile-aggregated counting-sort scatter: ranks inside a 2048-sample tile
     // come from shared-memory atomics; each (tile, bucket) reserves its slots
     // with ONE global atomic, so hot buckets are not serialised per warp.
-    constexpr int kItems = 8;
     constexpr int kTile = 256 * kItems;
     __shared__ unsigned int s_cnt[kMaxBuckets];
     __shared__ unsigned int s_base[kMaxBuckets];
@@ -840,11 +841,27 @@ cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* c
                                int forward, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint64_t blocks_needed = (n + 2047) / 2048;  // one 2048-sample tile per block pass
+    // items per thread: a larger tile gives the samples of one bucket longer
+    // runs of consecutive slots (longer contiguous record / map writes)
+    static const int items = [] {
+        const char* e = std::getenv("BMC_SCATTER_ITEMS");
+        const int v = e ? std::atoi(e) : 8;
+        return (v == 16 || v == 32) ? v : 8;
+    }();
+    const uint64_t tile = 256u * static_cast<uint64_t>(items);
+    const uint64_t blocks_needed = (n + tile - 1) / tile;
     const int grid = static_cast<int>(std::min<uint64_t>(blocks_needed,
                                                          static_cast<uint64_t>(sm_count_cached(dev)) * 8));
-    bin_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade, packed,
-                                            perm, forward);
+    if (items == 32) {
+        bin_scatter_kernel<32><<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade,
+                                                    packed, perm, forward);
+    } else if (items == 16) {
+        bin_scatter_kernel<16><<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade,
+                                                    packed, perm, forward);
+    } else {
+        bin_scatter_kernel<8><<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade,
+                                                   packed, perm, forward);
+    }
     return cudaGetLastError();
 }
 

@@ -424,31 +424,39 @@ class CudaExecutor:
         return self.min_safe_headways(d, hz, [risk])[0]
 
     def min_safe_headways(self, d, hz, risks: Sequence[float]):
+        """min_safe_headway per level through the fused statistics stage
+        (level-1 buckets, compaction, exact selection; 16 levels a call)."""
         n = int(d.numel())
         if n == 0:
             raise N.ConfigError("risk: needs at least one result")
-        ranks = []
         for risk in risks:
             if not (0.0 < risk < 1.0):
                 raise N.ConfigError("risk.level: must be strictly between 0 and 1")
-            raw = (1.0 - risk) * float(n)
-            ranks.append(int(math.ceil(raw - raw * 1e-12)))
-        vals, stopped = self.order_stats(d, hz, ranks, exclude_horizon=True)
-        return [float("inf") if rk > stopped else float(v) for rk, v in zip(ranks, vals)]
+        out = []
+        risks = list(risks)
+        for k0 in range(0, len(risks), 16):
+            out += [float(v) for v in self.stats(d, hz, risk_levels=risks[k0:k0 + 16])
+                    ["min_safe_headway"]]
+        return out
 
     def build_risk_curve(self, d, hz, grid: Sequence[float], risk_levels: Sequence[float],
                          closing_speed: float):
-        """build_risk_curve (analysis.cpp:203-228): one O(n log m) pass for the
-        whole grid instead of one O(n) rescan per grid point."""
+        """build_risk_curve (analysis.cpp:203-228): the whole grid's
+        exceedance counts and every threshold from one statistics stage
+        (the reference rescans the results once per grid point)."""
         n = float(d.numel())
-        counts = self.exceedance_counts(d, hz, grid)
+        levels = sorted(risk_levels, reverse=True)
+        if len(levels) <= 16:
+            out = self.stats(d, hz, headways=grid, risk_levels=levels)
+            counts, heads = out["exceed"], [float(v) for v in out["min_safe_headway"]]
+        else:
+            counts = self.exceedance_counts(d, hz, grid)
+            heads = self.min_safe_headways(d, hz, levels)
         probs = counts.astype(np.float64) / n
         g = list(grid)
         for i in range(1, len(g)):
             if g[i] >= g[i - 1] and probs[i] > probs[i - 1]:
                 raise AssertionError("risk curve must be non-increasing in headway")
-        levels = sorted(risk_levels, reverse=True)
-        heads = self.min_safe_headways(d, hz, levels)
         thr = [(r, h, ttc_for_headway(h, closing_speed)) for r, h in zip(levels, heads)]
         return probs, thr
 

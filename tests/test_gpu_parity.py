@@ -187,9 +187,9 @@ def test_device_resident_path(ref, executor):
     assert int(total.item()) == int(want["steps"].sum())
     rms, pms = executor.last_kernel_ms()
     assert rms > 0.0
-    # predict, scan, scatter, rollout (outputs written at each sample's index
-    # through the forward map: no unpermute pass unless BMC_UNPERMUTE=1)
-    assert executor.last_launches() == (5 if os.environ.get("BMC_UNPERMUTE") == "1" else 4)
+    # predict, scan, scatter, rollout, unpermute (BMC_DIRECT_OUTPUTS=1: the
+    # rollout writes each sample's outputs at its index, no unpermute pass)
+    assert executor.last_launches() == (4 if os.environ.get("BMC_DIRECT_OUTPUTS") == "1" else 5)
 
 
 def test_cpp_executor_api():
