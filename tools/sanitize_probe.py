@@ -38,10 +38,36 @@ h = ex.min_safe_headways(d, hz, [0.05, 0.01])
 noisy = ex.exceedance_ttc_noise(d, hz, [1.0 + 0.25 * k for k in range(21)], 30.0, 0.2, 9)
 assert noisy.tolist() == port.exceed_ttc_noise(want, [1.0 + 0.25 * k for k in range(21)], 30.0,
                                                0.2, 9).tolist()
+# fused statistics stage: pass 1 in the rollout epilogue (and standalone), pass 2,
+# targets, compaction, selection, the exact fallbacks (tiny candidate capacity
+# and a histogram wider than the device capacity), a statistics decision graph
+heads = [30.0 * (1 + 0.25 * k) for k in range(21)]
+stage = ex.stats_stage(n, heads, [0.05, 0.01, 0.001], summarize=True, bin_width=2.0)
+stage.begin()
+ex.rollout_device(dev, (d, st, hz), stats=stage)
+fused = stage.finish(d, hz)
+stage.close()
+one = ex.stats(d, hz, heads, [0.05, 0.01, 0.001], True, 2.0)
+assert fused["exceed"].tolist() == one["exceed"].tolist() == c.tolist()
+assert fused["summary"]["median"] == one["summary"]["median"] == s["median"]
+fb = ex.stats(d, hz, heads, [0.05, 0.01], True, 0.01, hist_cap=64, cand_cap=2)
+assert fb["fallbacks"] > 0 and fb["summary"]["median"] == s["median"]
+from paper_2604_27193_b200.stats import StatsRequest  # noqa: E402
+gs = ex.graph(2000, stats=StatsRequest(heads, [0.05], True, 2.0))
+gs.run(samples[:2000])
+gs.stats()
+gs.close()
 # device sampler, model-driven pipeline, decision graphs
 ex.draw_device(bmc.UncertaintyModel(seed=3), 5000)
 out = np.empty(4000, dtype=bmc.RESULT_DTYPE)
 ex.run_model(bmc.UncertaintyModel(seed=4), 4000, out=out, sampler="device")
+dd = torch.empty(4000, dtype=torch.float64, device="cuda")
+hh = torch.empty(4000, dtype=torch.uint8, device="cuda")
+stage = ex.stats_stage(4000, heads, [0.01], summarize=True)
+stage.begin()
+ex.run_model(bmc.UncertaintyModel(seed=4), 4000, device_out=(dd, None, hh), stats=stage, chunk=1500)
+assert stage.finish(dd, hh)["n"] == 4000
+stage.close()
 g = ex.graph(2000)
 g.run(samples[:2000])
 g.run_model(bmc.UncertaintyModel(seed=6))
