@@ -428,34 +428,12 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
         return BMC_OK;
     };
 
-    // Chunk schedule.  Only the first chunk's host staging + H2D and the last
-    // chunk's D2H + unpack are not overlapped with GPU work, so with the
-    // default chunk the edges ramp (chunk/8, /4, /2 ... /2, /4, /8): the GPU
-    // starts sooner and the exposed tail is an eighth of a chunk.  Results
-    // never depend on the schedule.
+    // Chunk schedule: fixed chunks.  (Ramping the first and last chunks down
+    // to chunk/8 to shorten the exposed staging / unpack was measured at 1e8
+    // and lost 7 ms per call -- each extra small chunk pays its own binning
+    // and rollout tail; tools/e2e_probe.py, profiles/round2_summary.md.)
     std::vector<std::pair<uint64_t, uint64_t>> sched;
-    {
-        std::vector<uint64_t> lens;
-        if (o.chunk_samples == 0 && chunk >= 8 && n >= 4 * chunk) {
-            const uint64_t ramp[3] = {chunk / 8, chunk / 4, chunk / 2};
-            const uint64_t edge = 2 * (ramp[0] + ramp[1] + ramp[2]);
-            for (uint64_t r : ramp) lens.push_back(r);
-            uint64_t mid = n - edge;
-            while (mid > 0) {
-                const uint64_t l = std::min(chunk, mid);
-                lens.push_back(l);
-                mid -= l;
-            }
-            for (int i = 2; i >= 0; --i) lens.push_back(ramp[i]);
-        } else {
-            for (uint64_t off = 0; off < n; off += chunk) lens.push_back(std::min(chunk, n - off));
-        }
-        uint64_t off = 0;
-        for (uint64_t l : lens) {
-            sched.emplace_back(off, l);
-            off += l;
-        }
-    }
+    for (uint64_t off = 0; off < n; off += chunk) sched.emplace_back(off, std::min(chunk, n - off));
     const uint64_t nchunks = sched.size();
     for (uint64_t k = 0; k < nchunks; ++k) {
         Slot& s = ctx->slots[k & 1];

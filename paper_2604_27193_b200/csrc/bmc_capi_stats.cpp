@@ -338,6 +338,8 @@ int stage_create(bmc_ctx* ctx, const bmc_stats_req* req, size_t max_n, bmc_stats
     st->L = make_layout(st->cfg);
     st->max_n = max_n;
     BMC_CK(ctx, st->mem.reserve(st->L.total * 8));
+    // every word defined (the read-back snapshot copies whole regions)
+    BMC_CK(ctx, cudaMemsetAsync(st->mem.p, 0, st->L.total * 8, ctx->stream));
     std::vector<uint64_t> consts(st->L.cand - st->L.headways, 0);
     if (st->cfg.m()) std::memcpy(consts.data(), st->cfg.headways.data(), st->cfg.headways.size() * 8);
     if (st->cfg.n_risk()) {

@@ -153,20 +153,20 @@ def test_beyond_1e8_samples_device_sampler(ref, executor):
         assert v == (math.inf if rank > stopped.size else np.partition(stopped, rank - 1)[rank - 1])
 
 
-def test_host_pipeline_ramped_chunks_bitwise(ref, executor):
-    """bmc_cuda_run above 8M samples ramps its chunk sizes at both ends
-    (chunk/8, /4, /2 ... /2, /4, /8): the results equal a fixed-chunk run
-    bit for bit and the reference on a random subset."""
+def test_host_pipeline_above_8m_bitwise(ref, executor):
+    """bmc_cuda_run above 8M samples (four pipeline chunks on two slot
+    streams): results equal a run with other chunk sizes bit for bit, and the
+    reference on a random subset."""
     n = 9_000_001
     samples, _ = bmc.draw_batch(bmc.UncertaintyModel(seed=5), n)
-    ramped = executor.run(samples)
-    assert ramped.chunks > 6  # 3 + middle + 3
-    fixed = executor.run(samples, chunk=1 << 21)
-    assert np.array_equal(ramped.results.view(np.uint8), fixed.results.view(np.uint8))
+    dflt = executor.run(samples)
+    assert dflt.chunks == 4
+    other = executor.run(samples, chunk=1 << 21)
+    assert np.array_equal(dflt.results.view(np.uint8), other.results.view(np.uint8))
     rng = np.random.default_rng(11)
     idx = np.sort(rng.choice(n, size=50_000, replace=False))
     want, _, _ = ref.run(np.ascontiguousarray(samples[idx]), World(), "parallel")
-    got = ramped.results[idx]
+    got = dflt.results[idx]
     assert np.array_equal(got["stop_distance"].view(np.uint64), want["stop_distance"].view(np.uint64))
     assert np.array_equal(got["steps"], want["steps"])
     assert np.array_equal(got["stop_time"].view(np.uint64), want["stop_time"].view(np.uint64))
