@@ -360,7 +360,8 @@ def parity_spot_check(bmc, args, samples, begin, d, st, hz, sw, out, dist, cdev,
     import torch
     from oracle.pyoracle import Reference, World
     n = samples.shape[0]
-    k = int(min(n, args.parity_samples))
+    world = dist.get_world_size() if dist is not None else 1
+    k = int(min(n, max(1, args.parity_samples // world)))  # the total is split over ranks
     rng = np.random.default_rng(20261017 + begin)
     idx = np.sort(rng.choice(n, size=k, replace=False)) if k < n else np.arange(n)
     ti = torch.from_numpy(idx).to(d.device)

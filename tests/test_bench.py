@@ -76,6 +76,21 @@ def test_b200_arm_two_ranks_gloo():
     assert lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0
     assert lines[0]["config"]["parallelism"] == "shard2"
     assert lines[0]["device_sampler"]["bit_identical_to_host_draw"]
+    # both ranks' spot checks against the reference, summed over ranks
+    assert lines[0]["parity"]["rollout_mismatches"] == 0
+    assert lines[0]["parity"]["rollouts_checked"] == 200000  # 1e5 per rank
+    # the merged statistics equal a one-process run of the same samples, bit
+    # for bit (exact partials), through five merge calls per step
+    st2 = lines[0]["statistics"]
+    assert st2["merge_calls_per_step"] == 5 and st2["fallbacks"] == 0
+    one = subprocess.run([sys.executable, "bench.py", "--samples", "2e5", "--steps", "2",
+                          "--warmup", "3", "--skip-cpu", "--skip-latency", "--skip-e2e"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert one.returncode == 0, one.stderr[-3000:]
+    (l1,) = _json_lines(one.stdout)
+    for k in ("n", "horizon_count", "collision_probability", "min_safe_headway_m", "mean", "sd",
+              "median", "skewness"):
+        assert st2[k] == l1["statistics"][k], k
 
 
 @pytest.mark.gpu
@@ -93,3 +108,5 @@ def test_b200_arm_nccl_torchrun_one_rank():
     assert p.returncode == 0, p.stderr[-3000:]
     (line,) = _json_lines(p.stdout)
     assert line["n_gpus"] == 1 and line["value"] > 0 and line["config"]["parallelism"] == "shard1"
+    assert line["statistics"]["merge_calls_per_step"] == 5  # NCCL through the stage's hooks
+    assert line["parity"]["rollout_mismatches"] == 0
