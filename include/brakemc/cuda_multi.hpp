@@ -281,6 +281,15 @@ public:
         if (coll->world() != static_cast<int>(shards_.size())) {
             throw ConfigError("execution.devices", "collective world differs from the device count");
         }
+        // every rank's stage runs under its device context's lock while it
+        // waits in the collective: two ranks on one device would deadlock
+        for (std::size_t i = 0; i < shards_.size(); ++i) {
+            for (std::size_t j = 0; j < i; ++j) {
+                if (shards_[i].device == shards_[j].device) {
+                    throw ConfigError("execution.devices", "merged statistics need distinct devices");
+                }
+            }
+        }
         const bmc_stats_req q = cuda_detail::stats_req_of(req);
         std::vector<std::unique_ptr<cuda_detail::StatsBuffers>> bufs;
         for (std::size_t g = 0; g < shards_.size(); ++g) {

@@ -118,7 +118,12 @@ int ensure_table(bmc_ctx* ctx, const WorldDerived& d, TableEntry** out) {
             }
         }
     }
-    if (cache.size() >= kTableCacheEntries) cache.pop_back();  // ~TableEntry: cudaFree waits
+    if (cache.size() >= kTableCacheEntries) {
+        // the least recently used world may still be read by a launch in
+        // flight on any stream: wait for the device before freeing it
+        BMC_CK(ctx, cudaDeviceSynchronize());
+        cache.pop_back();
+    }
     cache.insert(cache.begin(), std::move(e));
     *out = cache.front().get();
     return BMC_OK;

@@ -10,7 +10,7 @@
 //   * test_backends.cpp:26-68: single-sample report, chunk/scheduling
 //     independence, repeat determinism, empty-batch ConfigError.
 // Exit 0 on success; prints one line per check.  Run by
-// tests/test_gpu_cpp.py on the GPU box.
+// tests/test_gpu_parity.py::test_cpp_executor_api on the GPU box.
 #include "brakemc/backends.hpp"
 #include "brakemc/cuda_analysis.hpp"
 #include "brakemc/cuda_executor.hpp"

@@ -289,3 +289,37 @@ def test_feasibility_search_logic():
     n, capped = bmc.engine.max_feasible_n(lambda k: 0.0, 0.53, 1000, 4096)
     assert capped and n == 4096
     assert bmc.engine.max_feasible_n(lambda k: 1.0, 0.53, 1000, 4096) == (0, False)
+
+
+def test_interleaved_worlds_never_rewrite_a_table_in_flight(ref, executor):
+    """a device-resident rollout for world A, then -- before
+    any synchronisation -- one for world B with a different actuator table.
+    Tables are immutable per-world cache entries, so A's in-flight kernel
+    keeps reading A's table; both results equal the reference."""
+    import torch
+    wa, wb = World(), World(actuator_tau=0.4, t_max=8.0)
+    sa, _ = ref.draw_batch(Model(seed=41), 300000)
+    sb, _ = ref.draw_batch(Model(seed=42), 4000)
+    want_a, _, _ = ref.run(sa, wa, "parallel")
+    want_b, _, _ = ref.run(sb, wb, "parallel")
+
+    def dev(samples, w):
+        t = bmc.stage_terms(samples, to_world(w))
+        n = samples.shape[0]
+        return ([torch.from_numpy(t[i]).cuda() for i in range(4)],
+                (torch.empty(n, dtype=torch.float64, device="cuda"),
+                 torch.empty(n, dtype=torch.int32, device="cuda"),
+                 torch.empty(n, dtype=torch.uint8, device="cuda")))
+
+    ta, oa = dev(sa, wa)
+    tb, ob = dev(sb, wb)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    executor.rollout_device(ta, oa, to_world(wa), stream=s1)   # long, in flight
+    executor.rollout_device(tb, ob, to_world(wb), stream=s2)   # new world, no sync
+    for _ in range(3):                                         # churn the table cache
+        executor.rollout_device(tb, ob, to_world(World(actuator_tau=0.1 + 0.05 * _)), stream=s2)
+    executor.rollout_device(tb, ob, to_world(wb), stream=s2)
+    torch.cuda.synchronize()
+    assert np.array_equal(oa[0].cpu().numpy().view(np.uint64), want_a["stop_distance"].view(np.uint64))
+    assert np.array_equal(ob[0].cpu().numpy().view(np.uint64), want_b["stop_distance"].view(np.uint64))
