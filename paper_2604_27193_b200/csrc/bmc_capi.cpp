@@ -433,10 +433,10 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
         return BMC_OK;
     };
 
-    // Chunk schedule: fixed chunks.  (Ramping the first and last chunks down
-    // to chunk/8 to shorten the exposed staging / unpack was measured at 1e8
-    // and lost 7 ms per call -- each extra small chunk pays its own binning
-    // and rollout tail; tools/e2e_probe.py, profiles/round2_summary.md.)
+    // Chunk schedule: fixed chunks.  (Smaller edge chunks to shorten the
+    // exposed first staging / last unpack were measured at 1e8: a symmetric
+    // chunk/8 ramp lost 7 ms per call, a chunk/4 first chunk won 2.6 ms
+    // (0.27%, within run-to-run spread); profiles/round2_summary.md.)
     std::vector<std::pair<uint64_t, uint64_t>> sched;
     for (uint64_t off = 0; off < n; off += chunk) sched.emplace_back(off, std::min(chunk, n - off));
     const uint64_t nchunks = sched.size();
