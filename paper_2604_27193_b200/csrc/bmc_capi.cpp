@@ -283,6 +283,12 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
     ra.work_counter = sc.counter.as<unsigned int>();
     ra.counters = reinterpret_cast<unsigned long long*>(sc.counter.as<char>() + 8);
     if (p1) ra.p1 = *p1;
+    // BMC_PER_STEP_TEST=1 (A/B runs): every block folds every step's speed
+    static const bool per_step = [] {
+        const char* e = std::getenv("BMC_PER_STEP_TEST");
+        return e && e[0] == '1';
+    }();
+    ra.monotone_blocks = per_step ? 0 : 1;
     if (ev) BMC_CK(ctx, cudaEventRecord(ev->r0, s));
     if (n > 0) {
         BMC_CK(ctx, launch_rollout(ra, plan.mode, plan.bt, plan.ilp, plan.test_block, s));

@@ -303,6 +303,67 @@ __device__ __forceinline__ LaneOut run_table(const RolloutArgs& A, const StageA*
 // is amortised over two dependency chains: one table-row load feeds both.
 // BLK: the V1 and V3 loops use the blocked termination test of
 // steps_from_blocked (running minimum over both chains, exact replay).
+// First step n from which every stage brake value of this chain is <= G,
+// i.e. every RK4 stage acceleration b - D*s^2 - G is <= 0 (exactly also in
+// rounding: fl(fl(b - p) - G) <= fl(b - G) <= 0 for p >= 0).  The stage
+// brake is max(A_s[n], F) (the crossover form of clamp_brake) and every
+// stage sequence is non-increasing (host-checked), so the row maximum is
+// too: binary search.  INT_MAX when it never happens (F > G: a downhill
+// grade the brakes cannot hold, or NaN).
+template <int MODE>
+__device__ __forceinline__ int monotone_from(const StageA* tab, int len, double F, double G) {
+    if (!(F <= G)) return INT_MAX;
+    int lo = 0, hi = len;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const StageA s = load_stage<MODE>(tab, mid);
+        const double mx = fmax(fmax(s.a0, s.a1), fmax(s.a2, s.a3));
+        if (mx > G) {
+            lo = mid + 1;
+        } else {
+            hi = mid;
+        }
+    }
+    return lo == len ? INT_MAX : lo;
+}
+
+// Blocked steps of both chains.  PER_STEP: fold hi_word(v) of every step into
+// the running minimum (exact detection of the first v <= 0).  Otherwise only
+// the block's last speeds are tested: valid when every acceleration in the
+// block is <= 0 (monotone_from), because then v is non-increasing -- rounding
+// included: v + fl(h/6 * cv) with cv <= 0 -- so a speed that reached <= 0
+// inside the block is still <= 0 at its end, and the exact replay below
+// finds the first such step.  One integer op less per step: measured +1.2%
+// FP64-pipe utilisation (profiles/round2_summary.md).
+template <int MODE, bool PER_STEP>
+__device__ __forceinline__ int block_table(const RolloutArgs& A, const StageA* tab, Chain& a,
+                                           Chain& b, int32_t n, StageA& nx) {
+    int m = INT_MAX;
+#pragma unroll
+    for (int k = 0; k < kTestBlock; ++k) {
+        const StageA s = nx;
+        nx = load_stage<MODE>(tab, n + k + 1);  // n + k + 1 <= p1 <= head
+        rk4_xv(a.x, a.v, s.a0, s.a1, s.a2, s.a3, a.D, a.G, A.dt, A.half, A.sixth);
+        rk4_xv(b.x, b.v, s.a0, s.a1, s.a2, s.a3, b.D, b.G, A.dt, A.half, A.sixth);
+        if (PER_STEP) m = min(m, min(hi_word(a.v), hi_word(b.v)));
+    }
+    return PER_STEP ? m : min(hi_word(a.v), hi_word(b.v));
+}
+
+template <bool PER_STEP>
+__device__ __forceinline__ int block_const(const RolloutArgs& A, Chain& a, Chain& b, double a0,
+                                           double a1, double a2, double a3, double b0, double b1,
+                                           double b2, double b3) {
+    int m = INT_MAX;
+#pragma unroll
+    for (int k = 0; k < kTestBlock; ++k) {
+        rk4_xv(a.x, a.v, a0, a1, a2, a3, a.D, a.G, A.dt, A.half, A.sixth);
+        rk4_xv(b.x, b.v, b0, b1, b2, b3, b.D, b.G, A.dt, A.half, A.sixth);
+        if (PER_STEP) m = min(m, min(hi_word(a.v), hi_word(b.v)));
+    }
+    return PER_STEP ? m : min(hi_word(a.v), hi_word(b.v));
+}
+
 template <int MODE, bool BLK>
 __device__ __forceinline__ void run_table2(const RolloutArgs& A, const StageA* tab, int len,
                                            uint64_t j0, uint64_t j1, bool ok0, bool ok1,
@@ -316,6 +377,13 @@ __device__ __forceinline__ void run_table2(const RolloutArgs& A, const StageA* t
     const int lmax = max(ok0 ? chain_cmax(a) : INT_MIN, ok1 ? chain_cmax(b) : INT_MIN);
     const int p1 = min(__reduce_min_sync(0xffffffffu, lmin), head);
     const int p2 = max(min(__reduce_max_sync(0xffffffffu, lmax), head), p1);
+    // warp-uniform step from which the table blocks may test only their end
+    int ps = INT_MAX;
+    if (BLK && A.monotone_blocks) {
+        const int ma = ok0 ? monotone_from<MODE>(tab, len, a.F, a.G) : 0;
+        const int mb = ok1 ? monotone_from<MODE>(tab, len, b.F, b.G) : 0;
+        ps = __reduce_max_sync(0xffffffffu, max(ma, mb));
+    }
     int32_t n = 0;
     bool hit = false;
     if (n < p2) {
@@ -323,15 +391,8 @@ __device__ __forceinline__ void run_table2(const RolloutArgs& A, const StageA* t
         if (BLK) {
             for (; n + kTestBlock <= p1; n += kTestBlock) {
                 const double xa0 = a.x, va0 = a.v, xb0 = b.x, vb0 = b.v;
-                int m = INT_MAX;
-#pragma unroll
-                for (int k = 0; k < kTestBlock; ++k) {
-                    const StageA s = nx;
-                    nx = load_stage<MODE>(tab, n + k + 1);  // n + k + 1 <= p1 <= head
-                    rk4_xv(a.x, a.v, s.a0, s.a1, s.a2, s.a3, a.D, a.G, A.dt, A.half, A.sixth);
-                    rk4_xv(b.x, b.v, s.a0, s.a1, s.a2, s.a3, b.D, b.G, A.dt, A.half, A.sixth);
-                    m = min(m, min(hi_word(a.v), hi_word(b.v)));
-                }
+                const int m = n >= ps ? block_table<MODE, false>(A, tab, a, b, n, nx)
+                                      : block_table<MODE, true>(A, tab, a, b, n, nx);
                 if (m <= 0) {
                     a.x = xa0;
                     a.v = va0;
@@ -386,15 +447,14 @@ __device__ __forceinline__ void run_table2(const RolloutArgs& A, const StageA* t
         const double b0 = b.c0 <= n ? b.F : s.a0, b1 = b.c1 <= n ? b.F : s.a1;
         const double b2 = b.c2 <= n ? b.F : s.a2, b3 = b.c3 <= n ? b.F : s.a3;
         if (BLK) {
+            // the constant stage brakes are F or the table's last row: every
+            // one is <= G iff monotone_from found a step (warp-uniform; this
+            // region is entered by a divergent subset of lanes, no votes here)
+            const bool mono = ps != INT_MAX;
             for (; n + kTestBlock <= M; n += kTestBlock) {
                 const double xa0 = a.x, va0 = a.v, xb0 = b.x, vb0 = b.v;
-                int m = INT_MAX;
-#pragma unroll
-                for (int k = 0; k < kTestBlock; ++k) {
-                    rk4_xv(a.x, a.v, a0, a1, a2, a3, a.D, a.G, A.dt, A.half, A.sixth);
-                    rk4_xv(b.x, b.v, b0, b1, b2, b3, b.D, b.G, A.dt, A.half, A.sixth);
-                    m = min(m, min(hi_word(a.v), hi_word(b.v)));
-                }
+                const int m = mono ? block_const<false>(A, a, b, a0, a1, a2, a3, b0, b1, b2, b3)
+                                   : block_const<true>(A, a, b, a0, a1, a2, a3, b0, b1, b2, b3);
                 if (m <= 0) {
                     a.x = xa0;
                     a.v = va0;

@@ -50,6 +50,7 @@ struct RolloutArgs {
     const uint32_t* fwd;              // nullable: sorted slot -> sample index; outputs are then
                                       // written SoA at the sample's index (no unpermute pass)
     P1Args p1;                        // fused statistics pass 1 (p1.sum nullptr: off)
+    int32_t monotone_blocks;          // 1: blocks past monotone_from test only their end
 };
 
 struct PredictArgs {

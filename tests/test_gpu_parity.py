@@ -9,6 +9,7 @@ verify_consistency verdict `pass` with max_abs_deviation == 0.0.
 import math
 import os
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -95,6 +96,51 @@ def test_loop_variants_never_change_bits(ref, executor, ilp, block, tb, table, w
     rep = executor.run(samples, to_world(w), table=table, block_threads=block, ilp=ilp,
                        test_block=tb)
     assert_parity(ref, want, rep.results)
+
+
+# Grades around the point where the final brake just holds the car (F ~ G):
+# warps mix chains whose every stage acceleration is <= 0 (blocks past
+# monotone_from test only their last speed) with chains that never get there,
+# plus near-zero initial speeds that stop inside the first block.
+BOUNDARY_MODELS = [
+    Model(seed=41, mean=(12.0, 0.12, 0.10, 1500.0, 0.3), sd=(6.0, 0.06, 0.08, 300.0, 0.1)),
+    Model(seed=42, mean=(25.0, 0.10, -0.10, 1500.0, 0.3), sd=(8.0, 0.05, 0.10, 300.0, 0.1)),
+    Model(seed=43, mean=(0.3, 0.8, 0.0, 1500.0, 0.3), sd=(0.4, 0.2, 0.2, 100.0, 0.05)),
+]
+
+
+@pytest.mark.parametrize("m", BOUNDARY_MODELS, ids=["uphill", "downhill", "slow"])
+@pytest.mark.parametrize("ilp,block,tb,table", [(2, 640, 8, "shared"), (2, 768, 8, "global"),
+                                                (1, 1024, 8, "shared")])
+@pytest.mark.parametrize("w", [World(), World(t_max=2.0, actuator_tau=0.5)], ids=["default", "short"])
+def test_monotone_blocks_at_the_holding_boundary(ref, executor, m, ilp, block, tb, table, w):
+    samples, _ = ref.draw_batch(m, 6000)
+    want, _, _ = ref.run(samples, w, "parallel")
+    rep = executor.run(samples, to_world(w), table=table, block_threads=block, ilp=ilp,
+                       test_block=tb)
+    assert_parity(ref, want, rep.results)
+
+
+def test_monotone_blocks_equal_per_step_test():
+    """The last-speed-only block test vs the per-step running minimum
+    (BMC_PER_STEP_TEST=1, a separate process: the switch is read once)."""
+    code = (
+        "import hashlib, sys; sys.path.insert(0, %r)\n"
+        "import paper_2604_27193_b200 as bmc\n"
+        "ex = bmc.CudaExecutor(0)\n"
+        "h = hashlib.sha256()\n"
+        "for mdl in (bmc.UncertaintyModel.mixed(7), bmc.UncertaintyModel(seed=9)):\n"
+        "    s, _ = bmc.draw_batch(mdl, 300000)\n"
+        "    for t in ('shared', 'global'):\n"
+        "        h.update(ex.run(s, table=t).results.tobytes())\n"
+        "print(h.hexdigest())\n" % ROOT)
+    outs = []
+    for env in ({}, {"BMC_PER_STEP_TEST": "1"}):
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                           env={**os.environ, **env})
+        assert p.returncode == 0, p.stderr
+        outs.append(p.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1]
 
 
 @pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 257])
