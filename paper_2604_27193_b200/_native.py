@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libbrakemc_b200.so")
+# BMC_LIB_PATH: an A/B build of the same library (tools/ab_build.sh)
+LIB_PATH = os.environ.get("BMC_LIB_PATH") or os.path.join(PKG, "lib", "libbrakemc_b200.so")
 
 BMC_OK, BMC_E_CONFIG, BMC_E_DOMAIN, BMC_E_CUDA, BMC_E_NOMEM, BMC_E_RANGE, BMC_E_IO = (
     0, -1, -2, -3, -4, -5, -6)

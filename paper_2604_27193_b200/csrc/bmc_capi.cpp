@@ -115,6 +115,17 @@ int ensure_table(bmc_ctx* ctx, const WorldDerived& d, TableEntry** out) {
                                        cudaMemcpyHostToDevice));
                 e->coarse_len = static_cast<int>(coarse.size());
                 e->coarse_h = static_cast<float>(static_cast<double>(H) * d.dt);
+                // the transient: coarse steps until brake_accel stays within
+                // 1e-6 of its final value (the predictor solves the rest in
+                // closed form)
+                const float a_inf = coarse.back();
+                long long j = 2 * K;
+                while (j > 0 && std::fabs(coarse[static_cast<size_t>(j - 1)] - a_inf) <=
+                                    1e-6f * std::fabs(a_inf)) {
+                    --j;
+                }
+                e->coarse_steps = static_cast<int>((j + 1) / 2);
+                e->coarse_inf = a_inf;
             }
         }
     }
@@ -178,6 +189,8 @@ int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uin
     p.coarse = te->coarse.as<float>();
     p.coarse_len = te->coarse_len;
     p.coarse_h = te->coarse_h;
+    p.coarse_steps = te->coarse_steps;
+    p.coarse_inf = te->coarse_inf;
     *plan = p;
     return BMC_OK;
 }
@@ -239,6 +252,8 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
         pa.coarse_a = plan.coarse;
         pa.coarse_len = plan.coarse_len;
         pa.h = plan.coarse_h;
+        pa.coarse_steps = plan.coarse_steps;
+        pa.a_inf = plan.coarse_inf;
         pa.inv_dt = static_cast<float>(1.0 / d.dt);
         pa.max_steps = static_cast<int32_t>(d.max_steps);
         pa.bucket_width = bucket_width(d);

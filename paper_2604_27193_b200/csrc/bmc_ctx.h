@@ -109,6 +109,8 @@ struct Plan {
     const float* coarse = nullptr;
     int coarse_len = 0;
     float coarse_h = 0.0f;
+    int coarse_steps = 0;
+    float coarse_inf = 0.0f;
 };
 
 // One pipeline slot: its own compute stream and rollout scratch, so chunk
@@ -141,6 +143,8 @@ struct TableEntry {
     DevBuf table, coarse;
     int coarse_len = 0;
     float coarse_h = 0.0f;
+    int coarse_steps = 0;     // predictor: numeric coarse steps (transient)
+    float coarse_inf = 0.0f;  // predictor: brake_accel after the transient
     ~TableEntry() {
         table.release();
         coarse.release();

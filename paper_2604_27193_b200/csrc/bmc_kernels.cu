@@ -327,22 +327,28 @@ __device__ __forceinline__ int monotone_from(const StageA* tab, int len, double 
     return lo == len ? INT_MAX : lo;
 }
 
-// Blocked steps of both chains.  PER_STEP: fold hi_word(v) of every step into
-// the running minimum (exact detection of the first v <= 0).  Otherwise only
-// the block's last speeds are tested: valid when every acceleration in the
-// block is <= 0 (monotone_from), because then v is non-increasing -- rounding
-// included: v + fl(h/6 * cv) with cv <= 0 -- so a speed that reached <= 0
-// inside the block is still <= 0 at its end, and the exact replay below
-// finds the first such step.  One integer op less per step: measured +1.2%
-// FP64-pipe utilisation (profiles/round2_summary.md).
-template <int MODE, bool PER_STEP>
-__device__ __forceinline__ int block_table(const RolloutArgs& A, const StageA* tab, Chain& a,
-                                           Chain& b, int32_t n, StageA& nx) {
+// Blocked steps of both chains, L steps from row n.  PER_STEP: fold
+// hi_word(v) of every step into the running minimum (exact detection of the
+// first v <= 0).  Otherwise only the block's last speeds are tested: valid
+// when every acceleration in the block is <= 0 (monotone_from), because then
+// v is non-increasing -- rounding included: v + fl(h/6 * cv) with cv <= 0 --
+// so a speed that reached <= 0 inside the block is still <= 0 at its end, and
+// the exact replay finds the first such step.  The monotone blocks are also
+// longer (kMonoBlock): the FP64 pipe binds and every other instruction in the
+// loop (termination test, block bookkeeping) costs an issue cycle the pipe
+// would have used (profiles/round2_summary.md).
+#ifndef BMC_MONO_BLOCK
+#define BMC_MONO_BLOCK 16
+#endif
+constexpr int kMonoBlock = BMC_MONO_BLOCK;
+
+template <int MODE, int L, bool PER_STEP>
+__device__ __forceinline__ int block_table(const RolloutArgs& A, const StageA* row, Chain& a,
+                                           Chain& b) {
     int m = INT_MAX;
 #pragma unroll
-    for (int k = 0; k < kTestBlock; ++k) {
-        const StageA s = nx;
-        nx = load_stage<MODE>(tab, n + k + 1);  // n + k + 1 <= p1 <= head
+    for (int k = 0; k < L; ++k) {
+        const StageA s = load_stage<MODE>(row, k);
         rk4_xv(a.x, a.v, s.a0, s.a1, s.a2, s.a3, a.D, a.G, A.dt, A.half, A.sixth);
         rk4_xv(b.x, b.v, s.a0, s.a1, s.a2, s.a3, b.D, b.G, A.dt, A.half, A.sixth);
         if (PER_STEP) m = min(m, min(hi_word(a.v), hi_word(b.v)));
@@ -350,18 +356,53 @@ __device__ __forceinline__ int block_table(const RolloutArgs& A, const StageA* t
     return PER_STEP ? m : min(hi_word(a.v), hi_word(b.v));
 }
 
-template <bool PER_STEP>
+template <int L, bool PER_STEP>
 __device__ __forceinline__ int block_const(const RolloutArgs& A, Chain& a, Chain& b, double a0,
                                            double a1, double a2, double a3, double b0, double b1,
                                            double b2, double b3) {
     int m = INT_MAX;
 #pragma unroll
-    for (int k = 0; k < kTestBlock; ++k) {
+    for (int k = 0; k < L; ++k) {
         rk4_xv(a.x, a.v, a0, a1, a2, a3, a.D, a.G, A.dt, A.half, A.sixth);
         rk4_xv(b.x, b.v, b0, b1, b2, b3, b.D, b.G, A.dt, A.half, A.sixth);
         if (PER_STEP) m = min(m, min(hi_word(a.v), hi_word(b.v)));
     }
     return PER_STEP ? m : min(hi_word(a.v), hi_word(b.v));
+}
+
+// Exact replay of up to L table steps from row n after a block test fired:
+// true with n advanced to the first step where either chain's v <= 0;
+// false (a false alarm: positive subnormal) with the state at the block end.
+template <int MODE>
+__device__ __forceinline__ bool replay_table(const RolloutArgs& A, const StageA* tab, Chain& a,
+                                             Chain& b, int32_t& n, int L) {
+#pragma unroll 1
+    for (int k = 0; k < L; ++k) {
+        const StageA s = load_stage<MODE>(tab, n + k);
+        rk4_xv(a.x, a.v, s.a0, s.a1, s.a2, s.a3, a.D, a.G, A.dt, A.half, A.sixth);
+        rk4_xv(b.x, b.v, s.a0, s.a1, s.a2, s.a3, b.D, b.G, A.dt, A.half, A.sixth);
+        if (not_positive(a.v) | not_positive(b.v)) {
+            n += k;
+            return true;
+        }
+    }
+    return false;
+}
+
+__device__ __forceinline__ bool replay_const(const RolloutArgs& A, Chain& a, Chain& b,
+                                             int32_t& n, int L, double a0, double a1, double a2,
+                                             double a3, double b0, double b1, double b2,
+                                             double b3) {
+#pragma unroll 1
+    for (int k = 0; k < L; ++k) {
+        rk4_xv(a.x, a.v, a0, a1, a2, a3, a.D, a.G, A.dt, A.half, A.sixth);
+        rk4_xv(b.x, b.v, b0, b1, b2, b3, b.D, b.G, A.dt, A.half, A.sixth);
+        if (not_positive(a.v) | not_positive(b.v)) {
+            n += k;
+            return true;
+        }
+    }
+    return false;
 }
 
 template <int MODE, bool BLK>
@@ -387,32 +428,25 @@ __device__ __forceinline__ void run_table2(const RolloutArgs& A, const StageA* t
     int32_t n = 0;
     bool hit = false;
     if (n < p2) {
-        StageA nx = load_stage<MODE>(tab, 0);
         if (BLK) {
-            for (; n + kTestBlock <= p1; n += kTestBlock) {
+            // per-step test until the warp's chains are all monotone ...
+            for (; n < ps && n + kTestBlock <= p1; n += kTestBlock) {
                 const double xa0 = a.x, va0 = a.v, xb0 = b.x, vb0 = b.v;
-                const int m = n >= ps ? block_table<MODE, false>(A, tab, a, b, n, nx)
-                                      : block_table<MODE, true>(A, tab, a, b, n, nx);
-                if (m <= 0) {
-                    a.x = xa0;
-                    a.v = va0;
-                    b.x = xb0;
-                    b.v = vb0;
-#pragma unroll 1
-                    for (int k = 0; k < kTestBlock; ++k) {
-                        const StageA s = load_stage<MODE>(tab, n + k);
-                        rk4_xv(a.x, a.v, s.a0, s.a1, s.a2, s.a3, a.D, a.G, A.dt, A.half, A.sixth);
-                        rk4_xv(b.x, b.v, s.a0, s.a1, s.a2, s.a3, b.D, b.G, A.dt, A.half, A.sixth);
-                        if (not_positive(a.v) | not_positive(b.v)) {
-                            n += k;
-                            hit = true;
-                            break;
-                        }
-                    }
-                    if (hit) break;
+                if (block_table<MODE, kTestBlock, true>(A, tab + n, a, b) <= 0) {
+                    a.x = xa0, a.v = va0, b.x = xb0, b.v = vb0;
+                    if ((hit = replay_table<MODE>(A, tab, a, b, n, kTestBlock))) break;
+                }
+            }
+            // ... then longer blocks that test only their last speeds
+            for (; !hit && n + kMonoBlock <= p1; n += kMonoBlock) {
+                const double xa0 = a.x, va0 = a.v, xb0 = b.x, vb0 = b.v;
+                if (block_table<MODE, kMonoBlock, false>(A, tab + n, a, b) <= 0) {
+                    a.x = xa0, a.v = va0, b.x = xb0, b.v = vb0;
+                    if ((hit = replay_table<MODE>(A, tab, a, b, n, kMonoBlock))) break;
                 }
             }
         }
+        StageA nx = load_stage<MODE>(tab, n);
         for (; !hit && n < p1; ++n) {
             const StageA s = nx;
             nx = load_stage<MODE>(tab, n + 1);
@@ -450,27 +484,21 @@ __device__ __forceinline__ void run_table2(const RolloutArgs& A, const StageA* t
             // the constant stage brakes are F or the table's last row: every
             // one is <= G iff monotone_from found a step (warp-uniform; this
             // region is entered by a divergent subset of lanes, no votes here)
-            const bool mono = ps != INT_MAX;
-            for (; n + kTestBlock <= M; n += kTestBlock) {
-                const double xa0 = a.x, va0 = a.v, xb0 = b.x, vb0 = b.v;
-                const int m = mono ? block_const<false>(A, a, b, a0, a1, a2, a3, b0, b1, b2, b3)
-                                   : block_const<true>(A, a, b, a0, a1, a2, a3, b0, b1, b2, b3);
-                if (m <= 0) {
-                    a.x = xa0;
-                    a.v = va0;
-                    b.x = xb0;
-                    b.v = vb0;
-#pragma unroll 1
-                    for (int k = 0; k < kTestBlock; ++k) {
-                        rk4_xv(a.x, a.v, a0, a1, a2, a3, a.D, a.G, A.dt, A.half, A.sixth);
-                        rk4_xv(b.x, b.v, b0, b1, b2, b3, b.D, b.G, A.dt, A.half, A.sixth);
-                        if (not_positive(a.v) | not_positive(b.v)) {
-                            n += k;
-                            hit = true;
-                            break;
-                        }
+            if (ps != INT_MAX) {
+                for (; n + kMonoBlock <= M; n += kMonoBlock) {
+                    const double xa0 = a.x, va0 = a.v, xb0 = b.x, vb0 = b.v;
+                    if (block_const<kMonoBlock, false>(A, a, b, a0, a1, a2, a3, b0, b1, b2, b3) <= 0) {
+                        a.x = xa0, a.v = va0, b.x = xb0, b.v = vb0;
+                        if ((hit = replay_const(A, a, b, n, kMonoBlock, a0, a1, a2, a3, b0, b1, b2, b3))) break;
                     }
-                    if (hit) break;
+                }
+            } else {
+                for (; n + kTestBlock <= M; n += kTestBlock) {
+                    const double xa0 = a.x, va0 = a.v, xb0 = b.x, vb0 = b.v;
+                    if (block_const<kTestBlock, true>(A, a, b, a0, a1, a2, a3, b0, b1, b2, b3) <= 0) {
+                        a.x = xa0, a.v = va0, b.x = xb0, b.v = vb0;
+                        if ((hit = replay_const(A, a, b, n, kTestBlock, a0, a1, a2, a3, b0, b1, b2, b3))) break;
+                    }
                 }
             }
         }
@@ -613,9 +641,11 @@ __global__ void __launch_bounds__(BT, 1) rollout_kernel(const RolloutArgs A) {
 
 constexpr int kMaxBuckets = 4096;
 
-// FP32 coarse-step RK4 of the speed lane (brake_accel sampled from the exact
-// actuator table) -> predicted stop step -> bucket (descending).  Only the
-// schedule depends on this; results never do.
+// FP32 coarse-step RK4 of the speed lane through the actuator transient
+// (brake_accel sampled from the exact actuator table), then the stop time of
+// dv/dt = c - D v^2 with the final constant c = max(a_inf, F) - G in closed
+// form -> predicted stop step -> bucket (descending).  Only the schedule
+// depends on this; results never do.
 __global__ void __launch_bounds__(256) predict_kernel(const PredictArgs P) {
     extern __shared__ float s_a[];
     __shared__ unsigned int s_hist[kMaxBuckets];
@@ -623,8 +653,8 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictArgs P) {
     for (int i = threadIdx.x; i < P.buckets; i += blockDim.x) s_hist[i] = 0u;
     __syncthreads();
     const float h = P.h, hh = 0.5f * P.h, h6 = P.h / 6.0f;
-    const int last = P.coarse_len - 1;
-    const int kmax = (P.coarse_len - 1) / 2;  // coarse steps to the horizon
+    const int ks = P.coarse_steps;  // <= (coarse_len - 1) / 2
+    const float t_s = static_cast<float>(ks) * h;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P.n;
          i += stride) {
@@ -632,13 +662,13 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictArgs P) {
         const float F = static_cast<float>(P.brake_floor[i]);
         const float D = static_cast<float>(P.drag[i]);
         const float G = static_cast<float>(P.grade[i]);
-        int pred = P.max_steps;
+        float tstar = -1.0f;
         // scheduling only: FP32 with explicit FMAs (the file is -fmad=false)
         const float nD = -D;
         float b1 = fmaxf(s_a[0], F) - G;
-        for (int k = 0; k < kmax; ++k) {
-            const float b2 = fmaxf(s_a[min(2 * k + 1, last)], F) - G;
-            const float b4 = fmaxf(s_a[min(2 * k + 2, last)], F) - G;
+        for (int k = 0; k < ks; ++k) {
+            const float b2 = fmaxf(s_a[2 * k + 1], F) - G;
+            const float b4 = fmaxf(s_a[2 * k + 2], F) - G;
             const float k1 = __fmaf_rn(nD, v * v, b1);
             const float v2 = __fmaf_rn(hh, k1, v);
             const float k2 = __fmaf_rn(nD, v2 * v2, b2);
@@ -649,13 +679,21 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictArgs P) {
             const float vn = __fmaf_rn(h6, __fmaf_rn(2.0f, k2 + k3, k1 + k4), v);
             b1 = b4;
             if (vn <= 0.0f) {
-                const float frac = v / (v - vn);
-                const float tstar = (static_cast<float>(k) + frac) * h;
-                pred = static_cast<int>(ceilf(tstar * P.inv_dt));
+                tstar = (static_cast<float>(k) + v / (v - vn)) * h;
                 break;
             }
             v = vn;
         }
+        if (tstar < 0.0f) {
+            // constant brake: dv/dt = -(q + D v^2), q = G - max(a_inf, F)
+            const float q = G - fmaxf(P.a_inf, F);
+            if (q > 0.0f) {
+                const float r = sqrtf(q * D);
+                tstar = t_s + (r > 0.0f ? atanf(v * D / r) / r : v / q);
+            }
+        }
+        int pred = P.max_steps;
+        if (tstar >= 0.0f) pred = static_cast<int>(fminf(ceilf(tstar * P.inv_dt), 2e9f));
         pred = max(1, min(pred, P.max_steps));
         // key = (descending step bucket, clamp class): warps see one class,
         // so the never-clamping majority runs the select-free loop body

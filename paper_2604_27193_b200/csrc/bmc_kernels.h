@@ -62,6 +62,8 @@ struct PredictArgs {
     const float* coarse_a;  // brake_accel at t = k * h/2, k = 0..coarse_len-1
     int32_t coarse_len;
     float h;                // coarse step (s)
+    int32_t coarse_steps;   // coarse RK4 steps through the actuator transient
+    float a_inf;            // brake_accel after it (constant to float precision)
     float inv_dt;
     int32_t max_steps;
     int32_t bucket_width;   // steps per bucket

@@ -41,6 +41,8 @@ ex = bmc.CudaExecutor(0)
 peak, _ = ex.fp64_peak()
 tot = torch.zeros(1, dtype=torch.int64, device="cuda")
 outs, times = [], {v: [] for v in a.variants}
+bins = {v: [] for v in a.variants}
+lanes = {}
 ref_out = None
 for rep in range(a.reps):
     for v in a.variants:
@@ -51,6 +53,8 @@ for rep in range(a.reps):
         ex.sync()
         r, _ = ex.last_kernel_ms()
         times[v].append(r)
+        bins[v].append(ex.last_stage_ms()[0])
+        lanes[v] = ex.lane_efficiency()[2]
         if rep == 0:
             if ref_out is None:
                 ref_out = (d.clone(), st.clone())
@@ -62,4 +66,5 @@ steps = int(tot.item())
 for v in a.variants:
     b, m = min(times[v]), statistics.median(times[v])
     print(f"{a.model} n={n} {v:45s} best {b:9.3f} ms  median {m:9.3f} ms  "
-          f"exec {32 * steps / (b * 1e-3) / peak:.4f} of probe", flush=True)
+          f"exec {32 * steps / (b * 1e-3) / peak:.4f} of probe  binning {min(bins[v]):.3f} ms  "
+          f"lane efficiency {lanes[v]:.5f}", flush=True)
