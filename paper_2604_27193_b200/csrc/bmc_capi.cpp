@@ -6,9 +6,11 @@
 #include "bmc_ctx.h"
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -203,15 +205,26 @@ int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uin
 // forward map (no unpermute pass; 940.6 ms/step, but the scattered partial
 // writes cost 226 B/sample of read-modify-write traffic inside the rollout,
 // hidden under its FP64 bound).  profiles/round2_summary.md has both.
-bool unpermute_mode() {
-    static const bool on = [] {
+// The streamed pipeline (run_pipeline) writes directly: its chunk outputs
+// (13 B/sample, <= 64 MiB) stay in the 126 MB L2, so the scattered writes
+// merge there instead of costing DRAM read-modify-write, and a chunk's D2H
+// no longer waits for an unpermute that the next chunk's persistent rollout
+// would hold off the SMs.
+int env_direct_outputs() {
+    static const int v = [] {
         const char* e = std::getenv("BMC_DIRECT_OUTPUTS");
-        return !(e && e[0] == '1');
+        return (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : -1;
     }();
-    return on;
+    return v;
 }
+bool resolve_direct(int direct) {
+    if (env_direct_outputs() >= 0) return env_direct_outputs() == 1;
+    return direct == 1;
+}
+constexpr uint64_t kDirectChunkBytes = uint64_t{64} << 20;
+int pipeline_direct(uint64_t chunk) { return chunk * 13 <= kDirectChunkBytes ? 1 : 0; }
 
-int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n) {
+int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n, int direct) {
     // counter: [0] work counter (u32) | [8] executed steps | [16] lane slots
     BMC_CK(ctx, sc.counter.reserve(64));
     if (plan.sched == kScheduleBinned) {
@@ -220,24 +233,25 @@ int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n) {
         BMC_CK(ctx, sc.perm.reserve(m * sizeof(uint32_t)));  // forward (or inverse) permutation
         BMC_CK(ctx, sc.hist.reserve(4096 * sizeof(unsigned int)));
         BMC_CK(ctx, sc.packed_in.reserve(m * sizeof(PackedTerms)));
-        if (unpermute_mode()) BMC_CK(ctx, sc.packed_out.reserve(m * sizeof(PackedOut)));
+        if (!resolve_direct(direct)) BMC_CK(ctx, sc.packed_out.reserve(m * sizeof(PackedOut)));
     }
     return BMC_OK;
 }
 
 int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms& terms,
                     uint64_t n, const bmc_outputs& out, unsigned long long* total_steps_dev,
-                    cudaStream_t s, KernelEvents* ev, uint32_t* launches, const P1Args* p1) {
+                    cudaStream_t s, KernelEvents* ev, uint32_t* launches, const P1Args* p1,
+                    int direct) {
     if (n >= (uint64_t{1} << 32)) {
         return fail(ctx, BMC_E_CONFIG, "batch: at most 2^32-1 samples per device launch");
     }
-    int rc = reserve_scratch(ctx, sc, plan, n);
+    int rc = reserve_scratch(ctx, sc, plan, n, direct);
     if (rc != BMC_OK) return rc;
     const WorldDerived& d = plan.d;
     uint32_t nl = 0;
     bool packed = false;
     const bool any_out = out.stop_distance || out.steps || out.hit_horizon;
-    const bool direct_out = !unpermute_mode();
+    const bool direct_out = resolve_direct(direct);
     if (ev) ev->predicted = false;
     if (plan.sched == kScheduleBinned && n > 0) {
         const int buckets = bucket_count(d);
@@ -375,11 +389,26 @@ int finish_draw(bmc_ctx* ctx, const DevBuf& ctr, uint64_t* clamps) {
 
 namespace {
 
-// Chunked host<->device pipeline (2 slots): per chunk the host pool fills
+int trace_level() {
+    static const int v = [] {
+        const char* e = std::getenv("BMC_PIPE_TRACE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+// Chunked host<->device pipeline (3 slots): per chunk the host pool fills
 // pinned SoA terms (from AoS samples, or straight from the sampler), the
 // h2d stream copies them, the compute stream bins + rolls out, and either
 // the d2h stream returns the compact outputs for the host unpack, or the
 // kernel writes straight into caller-owned device outputs.
+// Why three: the persistent rollout of chunk k+1 takes every SM during the
+// tail of chunk k's rollout, so chunk k's unpermute (and with it its D2H)
+// only runs after chunk k+1's rollout.  With two slots the host, which must
+// unpack chunk k before staging chunk k+2 into the same slot, then left the
+// device idle ~9.5 ms every second chunk (BMC_PIPE_TRACE=2 timeline,
+// profiles/round2_summary.md); a third slot gives the host a whole chunk of
+// slack.
 int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const bmc_run_opts& o,
                  uint64_t n, const bmc_sample* samples, const bmc_model* model, uint64_t first,
                  bmc_result* host_out, const bmc_outputs* dev_out, bmc_run_info* info,
@@ -397,7 +426,15 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
         BMC_CK(ctx, ctx->draw_ctr.reserve(16));
         BMC_CK(ctx, cudaMemsetAsync(ctx->draw_ctr.p, 0, 16, ctx->stream));
     }
-    for (auto& s : ctx->slots) {
+    static const uint64_t kSlots = [] {  // BMC_PIPE_SLOTS=2 (A/B runs)
+        const char* e = std::getenv("BMC_PIPE_SLOTS");
+        return (e && e[0] == '2') ? uint64_t{2} : uint64_t{sizeof(bmc_ctx::slots) / sizeof(Slot)};
+    }();
+    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    const uint64_t used_slots = std::min(kSlots, nchunks);
+    const int direct = pipeline_direct(chunk);
+    for (uint64_t q = 0; q < used_slots; ++q) {
+        Slot& s = ctx->slots[q];
         if (!dev_draw) BMC_CK(ctx, s.h_terms.reserve(chunk * 32));
         BMC_CK(ctx, s.d_terms.reserve(chunk * 32));
         if (host_out) {
@@ -408,8 +445,8 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
     }
     BMC_CK(ctx, ctx->total_steps.reserve(sizeof(unsigned long long)));
     BMC_CK(ctx, cudaMemsetAsync(ctx->total_steps.p, 0, sizeof(unsigned long long), ctx->stream));
-    for (auto& s : ctx->slots) {
-        if ((rc = reserve_scratch(ctx, s.sc, plan, chunk)) != BMC_OK) return rc;
+    for (uint64_t q = 0; q < used_slots; ++q) {
+        if ((rc = reserve_scratch(ctx, ctx->slots[q].sc, plan, chunk, direct)) != BMC_OK) return rc;
     }
     // the slot streams start after the counters above are cleared
     BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
@@ -418,10 +455,37 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
     uint32_t launches = 0;
     std::atomic<uint64_t> clamps{0};
     const auto t0 = Clock::now();
+    // BMC_PIPE_TRACE=1: host-side phase totals of this call on stderr
+    // (waiting on the device, unpack, staging) -- diagnostics only
+    const bool trace = trace_level() >= 1;
+    double t_wait = 0.0, t_unpack = 0.0, t_stage = 0.0;
+    // BMC_PIPE_TRACE=2 adds the device timeline of every chunk (ms from the
+    // call's start): binning start/end, rollout start/end, unpermute end
+    cudaEvent_t base = nullptr;
+    std::vector<std::array<float, 6>> tl;
+    if (trace_level() >= 2) {
+        BMC_CK(ctx, cudaEventCreate(&base));
+        BMC_CK(ctx, cudaEventRecord(base, ctx->stream));
+    }
+    auto since = [](Clock::time_point a) { return std::chrono::duration<double>(Clock::now() - a).count(); };
 
     auto finish = [&](Slot& s) -> int {
         if (!s.busy) return BMC_OK;
+        auto tw = Clock::now();
         BMC_CK(ctx, cudaEventSynchronize(s.d2h_done));
+        t_wait += since(tw);
+        if (base) {
+            std::array<float, 6> r{};
+            r[0] = static_cast<float>(s.offset / chunk);
+            cudaEvent_t evs[5] = {s.kev.p0, s.kev.p1, s.kev.r0, s.kev.r1, s.kev.u1};
+            for (int q = 0; q < 5; ++q) {
+                const bool have = (q >= 2 || s.kev.predicted) && (q < 4 || s.kev.unpermuted);
+                r[q + 1] = -1.0f;
+                if (have) BMC_CK(ctx, cudaEventElapsedTime(&r[q + 1], base, evs[q]));
+            }
+            tl.push_back(r);
+        }
+        tw = Clock::now();
         float ms = 0.0f;
         BMC_CK(ctx, cudaEventElapsedTime(&ms, s.kev.r0, s.kev.r1));
         kernel_ms += ms;
@@ -450,6 +514,7 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
                 },
                 threads);
         }
+        t_unpack += since(tw);
         s.busy = false;
         return BMC_OK;
     };
@@ -460,9 +525,8 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
     // (0.27%, within run-to-run spread); profiles/round2_summary.md.)
     std::vector<std::pair<uint64_t, uint64_t>> sched;
     for (uint64_t off = 0; off < n; off += chunk) sched.emplace_back(off, std::min(chunk, n - off));
-    const uint64_t nchunks = sched.size();
     for (uint64_t k = 0; k < nchunks; ++k) {
-        Slot& s = ctx->slots[k & 1];
+        Slot& s = ctx->slots[k % kSlots];
         if ((rc = finish(s)) != BMC_OK) return rc;
         s.offset = sched[k].first;
         s.len = sched[k].second;
@@ -483,6 +547,7 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
             double* hfl = hv0 + s.len;
             double* hdr = hfl + s.len;
             double* hgr = hdr + s.len;
+            const auto ts = Clock::now();
             std::atomic<int> status{BMC_OK};
             ctx_pool(ctx, threads).parallel_for(
                 s.len,
@@ -500,6 +565,7 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
                     if (r != BMC_OK) status = r;
                 },
                 threads);
+            t_stage += since(ts);
             if (status != BMC_OK) {
                 for (auto& q : ctx->slots) cudaStreamSynchronize(q.compute);
                 cudaStreamSynchronize(ctx->d2h);
@@ -524,7 +590,7 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
         }
         rc = enqueue_rollout(ctx, plan, s.sc, terms, s.len, outs,
                              ctx->total_steps.as<unsigned long long>(), s.compute, &s.kev,
-                             &launches, p1);
+                             &launches, p1, direct);
         if (rc != BMC_OK) return rc;
         BMC_CK(ctx, cudaEventRecord(s.compute_done, s.compute));
         BMC_CK(ctx, cudaStreamWaitEvent(ctx->d2h, s.compute_done, 0));
@@ -535,14 +601,28 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
         BMC_CK(ctx, cudaEventRecord(s.d2h_done, ctx->d2h));
         s.busy = true;
     }
-    for (uint64_t k = nchunks > 2 ? nchunks - 2 : 0; k < nchunks; ++k) {
-        if ((rc = finish(ctx->slots[k & 1])) != BMC_OK) return rc;
+    for (uint64_t k = nchunks > kSlots ? nchunks - kSlots : 0; k < nchunks; ++k) {
+        if ((rc = finish(ctx->slots[k % kSlots])) != BMC_OK) return rc;
     }
     unsigned long long steps_total = 0;
     BMC_CK(ctx, cudaMemcpy(&steps_total, ctx->total_steps.p, sizeof steps_total, cudaMemcpyDeviceToHost));
     uint64_t dev_clamps = 0;
     if (dev_draw && (rc = finish_draw(ctx, ctx->draw_ctr, &dev_clamps)) != BMC_OK) return rc;
     const double wall = std::chrono::duration<double>(Clock::now() - t0).count();
+    if (trace) {
+        std::fprintf(stderr,
+                     "bmc pipe: n %llu chunks %llu threads %u wall %.2f ms | host: wait %.2f "
+                     "unpack %.2f stage %.2f ms | device: kernel %.2f predict %.2f ms\n",
+                     static_cast<unsigned long long>(n), static_cast<unsigned long long>(nchunks),
+                     threads, wall * 1e3, t_wait * 1e3, t_unpack * 1e3, t_stage * 1e3, kernel_ms,
+                     predict_ms);
+        for (const auto& r : tl) {
+            std::fprintf(stderr,
+                         "  chunk %3d  bin %8.2f..%8.2f  rollout %8.2f..%8.2f (%6.2f)  unpermute ..%8.2f\n",
+                         static_cast<int>(r[0]), r[1], r[2], r[3], r[4], r[4] - r[3], r[5]);
+        }
+    }
+    if (base) cudaEventDestroy(base);
     ctx->last_launches = launches;
     if (clamp_count) *clamp_count = dev_draw ? dev_clamps : clamps.load();
     if (info) {
@@ -853,7 +933,7 @@ int bmc_cuda_run_model_stats(bmc_ctx* ctx, const bmc_model* model, uint64_t firs
             return fail(ctx, BMC_E_CONFIG, "stats: more results than the stage was sized for");
         }
     }
-    // chunks run on the two slot streams; the stage was begun on ctx->stream,
+    // chunks run on the slot streams; the stage was begun on ctx->stream,
     // which run_pipeline synchronises before the first chunk
     return bmc::run_pipeline(ctx, *world, d, o, n, nullptr, model, first, host_out, dev_out, info,
                              clamp_count, st ? &p1 : nullptr);

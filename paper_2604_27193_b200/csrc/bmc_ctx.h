@@ -184,7 +184,9 @@ struct bmc_ctx {
     // the stage bmc_cuda_stats reuses while the request and size class match
     bmc_stats_stage* stats_cache = nullptr;
 
-    bmc::Slot slots[2];
+    // pipeline slots (bmc_capi.cpp run_pipeline): three, so a chunk's host
+    // staging never waits on the chunk the device finished last
+    bmc::Slot slots[3];
     bmc::DevBuf partials, sel_hist, sel_pref, sorted_h, buckets, hist_buf;
 };
 
@@ -220,7 +222,10 @@ int ensure_table(bmc_ctx* ctx, const WorldDerived& d, TableEntry** out);
 ThreadPool& ctx_pool(bmc_ctx* ctx, unsigned threads);
 int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uint64_t n,
               Plan* plan);
-int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n);
+// Output path of a binned launch: -1 = the default (packed sorted records +
+// unpermute; BMC_DIRECT_OUTPUTS=1 flips it), 0 = packed + unpermute,
+// 1 = direct writes at each sample's index through the forward map.
+int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n, int direct = -1);
 // Device sampler (bmc_capi.cpp): resolve bmc_run_opts.sampler to a yes/no.
 int use_device_sampler(bmc_ctx* ctx, const bmc_run_opts& o, bool* device);
 // Fill DrawArgs from a model + world (no output pointers set).
@@ -252,7 +257,7 @@ size_t stats_max_n(const bmc_stats_stage* st);
 int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms& terms,
                     uint64_t n, const bmc_outputs& out, unsigned long long* total_steps_dev,
                     cudaStream_t s, KernelEvents* ev, uint32_t* launches,
-                    const P1Args* p1 = nullptr);
+                    const P1Args* p1 = nullptr, int direct = -1);
 // Legacy statistics calls run on ctx->stream: order them after the last
 // device-resident rollout, whatever stream it was enqueued on.
 inline int order_after_rollouts(bmc_ctx* ctx) {
