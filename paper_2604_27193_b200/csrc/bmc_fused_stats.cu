@@ -24,6 +24,62 @@ int grid_for(uint64_t n, int sms, int per_sm, int threads) {
     return static_cast<int>(need < 1 ? 1 : (need < cap ? need : cap));
 }
 
+// Streaming loop over (d[i], hz[i]): when d is 16-B and hz 4-B aligned, each
+// thread takes groups of 4 consecutive results (two 16-B loads + one 4-B
+// load), kGroups groups in flight, consecutive threads on consecutive groups
+// -- a warp reads 1 KB of d contiguously (ncu: the strided 8-B form left
+// pass 2 at 0.83 TB/s and compaction at 1.35 TB/s).  f(i, v, h) per result;
+// LOAD_HZ false passes h = 0 and leaves hz to f.
+#ifndef BMC_STREAM_LD
+#define BMC_STREAM_LD 0
+#endif
+template <class T>
+__device__ __forceinline__ T stream_ld(const T* p) {
+    if (BMC_STREAM_LD == 1) return __ldg(p);
+    if (BMC_STREAM_LD == 2) return *p;
+    return __ldcs(p);
+}
+// Software-pipelined: the next group's loads are issued before the current
+// group is processed (the per-result work ends in atomics / stores the
+// compiler cannot hoist later loads above).
+template <bool LOAD_HZ, class F>
+__device__ __forceinline__ void stream_results(const double* d, const uint8_t* hz, uint64_t n, F&& f) {
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const bool vec = (reinterpret_cast<uintptr_t>(d) & 15u) == 0 &&
+                     (!LOAD_HZ || hz == nullptr || (reinterpret_cast<uintptr_t>(hz) & 3u) == 0);
+    if (!vec) {
+        for (uint64_t i = tid; i < n; i += stride) f(i, d[i], LOAD_HZ && hz != nullptr ? hz[i] : 0);
+        return;
+    }
+    const uint64_t ng = n / 4;
+    const double2* d2 = reinterpret_cast<const double2*>(d);
+    const uint32_t* h4 = reinterpret_cast<const uint32_t*>(hz);
+    uint64_t g = tid;
+    double2 a = make_double2(0.0, 0.0), b = a;
+    uint32_t h = 0u;
+    if (g < ng) {
+        a = stream_ld(d2 + 2 * g);
+        b = stream_ld(d2 + 2 * g + 1);
+        if (LOAD_HZ && hz != nullptr) h = stream_ld(h4 + g);
+    }
+    for (; g < ng; g += stride) {
+        const double2 ca = a, cb = b;
+        const uint32_t ch = h;
+        const uint64_t gn = g + stride;
+        if (gn < ng) {
+            a = stream_ld(d2 + 2 * gn);
+            b = stream_ld(d2 + 2 * gn + 1);
+            if (LOAD_HZ && hz != nullptr) h = stream_ld(h4 + gn);
+        }
+        f(4 * g, ca.x, ch & 0xffu);
+        f(4 * g + 1, ca.y, (ch >> 8) & 0xffu);
+        f(4 * g + 2, cb.x, (ch >> 16) & 0xffu);
+        f(4 * g + 3, cb.y, ch >> 24);
+    }
+    for (uint64_t i = 4 * ng + tid; i < n; i += stride) f(i, d[i], LOAD_HZ && hz != nullptr ? hz[i] : 0);
+}
+
 // Per-thread register window over kWin consecutive limbs of one exact sum
 // (one sign).  A value whose three limb contributions fall inside the
 // window adds to registers; otherwise the window is flushed to the CTA's
@@ -216,10 +272,21 @@ struct P2Smem {
 // Pass 2 (needs the merged P1 scalars): exact m2/m3 (analysis.cpp:39-46,
 // dev*dev and (dev*dev)*dev rounded as written), the summarize histogram
 // (:64-75) and the level-1 order-statistic histograms (all / stoppers).
-constexpr int kPass2Threads = 512;
-constexpr int kUnroll = 4;
+// 256 threads x 3 CTAs per SM (80 registers): 875 us at 1e8 against 1.09 ms
+// for 512 x 1 (122 registers), ncu, profiles/round2_hbm_stage_ab.txt
+#ifndef BMC_P2_THREADS
+#define BMC_P2_THREADS 256
+#endif
+#ifndef BMC_P2_MINB
+#define BMC_P2_MINB 3
+#endif
+#ifndef BMC_P2_VEC
+#define BMC_P2_VEC 0
+#endif
+constexpr int kPass2Threads = BMC_P2_THREADS;
+constexpr int kPass2MinBlocks = BMC_P2_MINB;
 
-__global__ void __launch_bounds__(kPass2Threads, 1) pass2_kernel(const double* d, const uint8_t* hz,
+__global__ void __launch_bounds__(kPass2Threads, kPass2MinBlocks) pass2_kernel(const double* d, const uint8_t* hz,
                                                                  uint64_t n, StageDev g) {
     extern __shared__ __align__(16) unsigned char sm[];
     P2Smem* S = reinterpret_cast<P2Smem*>(sm);
@@ -262,22 +329,26 @@ __global__ void __launch_bounds__(kPass2Threads, 1) pass2_kernel(const double* d
         atomicAdd(&S->sel_all[b], 1u);
         if (!h) atomicAdd(&S->sel_stop[b], 1u);
     };
-    // kUnroll independent loads in flight per thread (the pass is latency-
-    // bound on its streaming reads, not on arithmetic)
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
-        double v[kUnroll];
-        uint8_t h[kUnroll];
+    if (BMC_P2_VEC) {
+        stream_results<true>(d, hz, n, [&](uint64_t, double v, unsigned h) { one(v, h != 0); });
+    } else {
+        // four independent strided loads in flight per thread
+        constexpr int kUnroll = 4;
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+            double v[kUnroll];
+            uint8_t h[kUnroll];
 #pragma unroll
-        for (int k = 0; k < kUnroll; ++k) {
-            v[k] = __ldcs(d + i + k * stride);
-            h[k] = hz != nullptr ? __ldcs(hz + i + k * stride) : 0;
+            for (int k = 0; k < kUnroll; ++k) {
+                v[k] = __ldcs(d + i + k * stride);
+                h[k] = hz != nullptr ? __ldcs(hz + i + k * stride) : 0;
+            }
+#pragma unroll
+            for (int k = 0; k < kUnroll; ++k) one(v[k], h[k] != 0);
         }
-#pragma unroll
-        for (int k = 0; k < kUnroll; ++k) one(v[k], h[k] != 0);
+        for (; i < n; i += stride) one(d[i], hz != nullptr && hz[i] != 0);
     }
-    for (; i < n; i += stride) one(d[i], hz != nullptr && hz[i] != 0);
     racc_flush(m2, S->acc);
     racc_flush(m3, S->acc + sc::kAccWords);
     __syncthreads();
@@ -366,14 +437,22 @@ __global__ void __launch_bounds__(kTargetThreads) targets_kernel(StageDev g) {
 // Values in each target's bucket -> that target's candidate list (order
 // keys).  A 4096-bit shared bitmap of the target buckets rejects almost
 // every value with one shared load; hit_horizon is read only on a hit.
+// Hits (~1e-3 of the values, ~1e5 at 1e8) gather in a per-CTA shared buffer
+// and reserve their global slots with one atomic per target per CTA: one
+// same-address global atomic per hit serialised in L2.
+constexpr int kCandBuf = 128;
 __global__ void __launch_bounds__(256) compact_kernel(const double* d, const uint8_t* hz, uint64_t n,
                                                       StageDev g) {
     __shared__ int s_bucket[sc::kMaxTargets];
     __shared__ int s_pop[sc::kMaxTargets];
     __shared__ unsigned s_map[sc::kB1 / 32];
+    __shared__ unsigned s_cnt[sc::kMaxTargets];
+    __shared__ unsigned long long s_base[sc::kMaxTargets];
+    __shared__ unsigned long long s_buf[sc::kMaxTargets][kCandBuf];
     __shared__ int s_T;
     const sc::Scalars s = *reinterpret_cast<const sc::Scalars*>(g.w + g.scal);
     for (int i = threadIdx.x; i < sc::kB1 / 32; i += blockDim.x) s_map[i] = 0u;
+    if (threadIdx.x < sc::kMaxTargets) s_cnt[threadIdx.x] = 0u;
     __syncthreads();
     if (threadIdx.x == 0) {
         const sc::Target* tg = reinterpret_cast<const sc::Target*>(g.w + g.targets);
@@ -398,22 +477,32 @@ __global__ void __launch_bounds__(256) compact_kernel(const double* d, const uin
         const int b = sc::sel_bucket(v, s.sel_lo, s.sel_scale);  // NaN -> bucket 0, filtered below
         if (!((s_map[b >> 5] >> (b & 31)) & 1u) || sc::is_nan(v)) return;
         const bool h = hz != nullptr && hz[i] != 0;
+        const unsigned long long key = sc::order_key(v);
         for (int t = 0; t < T; ++t) {
             if (s_bucket[t] != b || (s_pop[t] == 1 && h)) continue;
-            const unsigned long long pos = atomicAdd(&cnt[t], 1ull);
-            if (pos < g.cand_cap) cand[static_cast<uint64_t>(t) * g.cand_cap + pos] = sc::order_key(v);
+            const unsigned p = atomicAdd(&s_cnt[t], 1u);
+            if (p < kCandBuf) {
+                s_buf[t][p] = key;
+            } else {  // buffer full: straight to the global list
+                const unsigned long long pos = atomicAdd(&cnt[t], 1ull);
+                if (pos < g.cand_cap) cand[static_cast<uint64_t>(t) * g.cand_cap + pos] = key;
+            }
         }
     };
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
-        double v[kUnroll];
-#pragma unroll
-        for (int k = 0; k < kUnroll; ++k) v[k] = __ldcs(d + i + k * stride);
-#pragma unroll
-        for (int k = 0; k < kUnroll; ++k) one(i + k * stride, v[k]);
+    stream_results<false>(d, hz, n, [&](uint64_t i, double v, unsigned) { one(i, v); });
+    __syncthreads();
+    if (threadIdx.x < T) {
+        const unsigned c = min(s_cnt[threadIdx.x], static_cast<unsigned>(kCandBuf));
+        s_base[threadIdx.x] = c ? atomicAdd(&cnt[threadIdx.x], static_cast<unsigned long long>(c)) : 0ull;
     }
-    for (; i < n; i += stride) one(i, d[i]);
+    __syncthreads();
+    for (int t = 0; t < T; ++t) {
+        const unsigned c = min(s_cnt[t], static_cast<unsigned>(kCandBuf));
+        for (unsigned j = threadIdx.x; j < c; j += blockDim.x) {
+            const unsigned long long pos = s_base[t] + j;
+            if (pos < g.cand_cap) cand[static_cast<uint64_t>(t) * g.cand_cap + pos] = s_buf[t][j];
+        }
+    }
 }
 
 // Local candidates -> one padded block [t0: P0][t1: P1]... (UINT64_MAX pads).
@@ -587,7 +676,7 @@ cudaError_t launch_pass2(const double* d, const uint8_t* hz, uint64_t n, const S
     cudaError_t e = cudaFuncSetAttribute(pass2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    pass2_kernel<<<grid_for(n, sms, 1, kPass2Threads), kPass2Threads, smem, s>>>(d, hz, n, g);
+    pass2_kernel<<<grid_for(n, sms, kPass2MinBlocks, kPass2Threads), kPass2Threads, smem, s>>>(d, hz, n, g);
     return cudaGetLastError();
 }
 

@@ -727,30 +727,48 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(unsigned int* hist, int 
     }
 }
 
+#ifndef BMC_SCATTER_PRELOAD
+#define BMC_SCATTER_PRELOAD 1
+#endif
 template <int kItems>
-__global__ void __launch_bounds__(256) bin_scatter_kernel(const uint16_t* keys, uint64_t n,
-                                                          unsigned int* cursor, const double* v0,
-                                                          const double* floor_, const double* drag,
-                                                          const double* grade, PackedTerms* packed,
-                                                          uint32_t* perm, int forward) {
+__global__ void __launch_bounds__(256, BMC_SCATTER_PRELOAD ? 2 : 1)
+    bin_scatter_kernel(const uint16_t* keys, uint64_t n, unsigned int* cursor, const double* v0,
+                       const double* floor_, const double* drag, const double* grade,
+                       PackedTerms* packed, uint32_t* perm, int forward) {
     // Tile-aggregated counting-sort scatter: ranks inside a 2048-sample tile
     // come from shared-memory atomics; each (tile, bucket) reserves its slots
     // with ONE global atomic, so hot buckets are not serialised per warp.
+    // The tile's keys AND terms are loaded into registers first, so their
+    // DRAM latency overlaps the shared-memory ranking and the bucket
+    // reservations (loaded after them, each item's four term loads waited
+    // behind the previous item's scattered stores: 1.5 TB/s, ncu).
     constexpr int kTile = 256 * kItems;
     __shared__ unsigned int s_cnt[kMaxBuckets];
     __shared__ unsigned int s_base[kMaxBuckets];
     for (uint64_t tile = static_cast<uint64_t>(blockIdx.x) * kTile; tile < n;
          tile += static_cast<uint64_t>(gridDim.x) * kTile) {
-        for (int b = threadIdx.x; b < kMaxBuckets; b += 256) s_cnt[b] = 0u;
-        __syncthreads();
         unsigned key[kItems], rank[kItems];
+        double tv[BMC_SCATTER_PRELOAD ? kItems : 1], tf[BMC_SCATTER_PRELOAD ? kItems : 1];
+        double td[BMC_SCATTER_PRELOAD ? kItems : 1], tg[BMC_SCATTER_PRELOAD ? kItems : 1];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
             const uint64_t i = tile + static_cast<uint64_t>(k) * 256 + threadIdx.x;
             if (i < n) {
                 key[k] = keys[i];
-                rank[k] = atomicAdd(&s_cnt[key[k]], 1u);
+                if (BMC_SCATTER_PRELOAD) {
+                    tv[k] = __ldcs(v0 + i);
+                    tf[k] = __ldcs(floor_ + i);
+                    td[k] = __ldcs(drag + i);
+                    tg[k] = __ldcs(grade + i);
+                }
             }
+        }
+        for (int b = threadIdx.x; b < kMaxBuckets; b += 256) s_cnt[b] = 0u;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            const uint64_t i = tile + static_cast<uint64_t>(k) * 256 + threadIdx.x;
+            if (i < n) rank[k] = atomicAdd(&s_cnt[key[k]], 1u);
         }
         __syncthreads();
         for (int b = threadIdx.x; b < kMaxBuckets; b += 256) {
@@ -770,8 +788,13 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(const uint16_t* keys, 
                 }
                 // one aligned 32-byte record = one full sector: no read-for-fill
                 double2* dst = reinterpret_cast<double2*>(packed + pos);
-                dst[0] = make_double2(v0[i], floor_[i]);
-                dst[1] = make_double2(drag[i], grade[i]);
+                if (BMC_SCATTER_PRELOAD) {
+                    dst[0] = make_double2(tv[k], tf[k]);
+                    dst[1] = make_double2(td[k], tg[k]);
+                } else {
+                    dst[0] = make_double2(v0[i], floor_[i]);
+                    dst[1] = make_double2(drag[i], grade[i]);
+                }
             }
         }
         __syncthreads();
@@ -939,27 +962,14 @@ cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* c
                                int forward, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
-    // items per thread: a larger tile gives the samples of one bucket longer
-    // runs of consecutive slots (longer contiguous record / map writes)
-    static const int items = [] {
-        const char* e = std::getenv("BMC_SCATTER_ITEMS");
-        const int v = e ? std::atoi(e) : 8;
-        return (v == 16 || v == 32) ? v : 8;
-    }();
-    const uint64_t tile = 256u * static_cast<uint64_t>(items);
+    // 8 items per thread (2048-sample tiles); 16 and 32 were measured slower
+    // (profiles/round2_summary.md, A/B table)
+    constexpr uint64_t tile = 256u * 8u;
     const uint64_t blocks_needed = (n + tile - 1) / tile;
     const int grid = static_cast<int>(std::min<uint64_t>(blocks_needed,
                                                          static_cast<uint64_t>(sm_count_cached(dev)) * 8));
-    if (items == 32) {
-        bin_scatter_kernel<32><<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade,
-                                                    packed, perm, forward);
-    } else if (items == 16) {
-        bin_scatter_kernel<16><<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade,
-                                                    packed, perm, forward);
-    } else {
-        bin_scatter_kernel<8><<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade,
-                                                   packed, perm, forward);
-    }
+    bin_scatter_kernel<8><<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade, packed,
+                                               perm, forward);
     return cudaGetLastError();
 }
 
