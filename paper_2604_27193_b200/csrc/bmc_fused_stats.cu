@@ -119,15 +119,11 @@ __device__ __forceinline__ void win_add(RegWin& r, unsigned long long* limbs, in
         r.L0 = min(max(L - 1, 0), sc::kLimbs - kWin);
         off = L - r.L0;
     }
-    if (off == 1) {
-        r.w[1] += w0;
-        r.w[2] += w1;
-        r.w[3] += w2;
-    } else {
-        r.w[0] += w0;
-        r.w[1] += w1;
-        r.w[2] += w2;
-    }
+    const bool hi = off == 1;
+    r.w[0] += hi ? 0u : w0;
+    r.w[1] += hi ? w0 : w1;
+    r.w[2] += hi ? w1 : w2;
+    r.w[3] += hi ? w2 : 0u;
 }
 
 // One exact sum's per-thread state: a window per sign + special counts.
@@ -158,6 +154,76 @@ __device__ __forceinline__ void racc_add(RegAcc& a, unsigned long long* acc, dou
     } else {
         win_add(a.pos, acc, L, w0, w1, w2);
     }
+}
+
+// A signed sum (m3: (dev*dev)*dev) in ONE window of signed limbs: a negative
+// term subtracts its limb words, so the sign never splits the warp (two
+// windows, one per sign, ran both paths for ~half the lanes each: ncu
+// showed the m3 update at 16 active threads).  At the flush a positive
+// limb adds to the CTA's positive limbs and a negative one to the negative
+// limbs -- the same exact value.  int64 limbs: < 2^31 terms per thread.
+struct RegWinS {
+    int L0;
+    long long w[kWin];
+};
+struct RegAccS {
+    RegWinS win;
+    unsigned long long nan, pinf, ninf;
+};
+
+__device__ __forceinline__ void wins_flush(RegWinS& r, unsigned long long* acc) {
+    if (r.L0 >= 0) {
+#pragma unroll
+        for (int k = 0; k < kWin; ++k) {
+            const long long v = r.w[k];
+            if (v > 0) atomicAdd(&acc[r.L0 + k], static_cast<unsigned long long>(v));
+            if (v < 0) atomicAdd(&acc[sc::kLimbs + r.L0 + k], static_cast<unsigned long long>(-v));
+            r.w[k] = 0;
+        }
+    }
+}
+
+__device__ __forceinline__ void racc_init(RegAccS& a) {
+    a.win.L0 = -1000;
+#pragma unroll
+    for (int k = 0; k < kWin; ++k) a.win.w[k] = 0;
+    a.nan = a.pinf = a.ninf = 0ull;
+}
+
+__device__ __forceinline__ void racc_add(RegAccS& a, unsigned long long* acc, double v) {
+    const int sp = sc::special_of(v);
+    if (sp != sc::kFinite) {
+        a.nan += sp == sc::kNaN ? 1ull : 0ull;
+        a.pinf += sp == sc::kPosInf ? 1ull : 0ull;
+        a.ninf += sp == sc::kNegInf ? 1ull : 0ull;
+        return;
+    }
+    int L;
+    uint32_t w0, w1, w2;
+    sc::split(v, &L, &w0, &w1, &w2);
+    const bool neg = (sc::bits_of(v) >> 63) != 0;
+    const long long s0 = neg ? -static_cast<long long>(w0) : static_cast<long long>(w0);
+    const long long s1 = neg ? -static_cast<long long>(w1) : static_cast<long long>(w1);
+    const long long s2 = neg ? -static_cast<long long>(w2) : static_cast<long long>(w2);
+    RegWinS& r = a.win;
+    int off = L - r.L0;
+    if (off != 1 && off != 0) {
+        wins_flush(r, acc);
+        r.L0 = min(max(L - 1, 0), sc::kLimbs - kWin);
+        off = L - r.L0;
+    }
+    const bool hi = off == 1;  // straight-line: both offsets as selects
+    r.w[0] += hi ? 0 : s0;
+    r.w[1] += hi ? s0 : s1;
+    r.w[2] += hi ? s1 : s2;
+    r.w[3] += hi ? s2 : 0;
+}
+
+__device__ __forceinline__ void racc_flush(RegAccS& a, unsigned long long* acc) {
+    wins_flush(a.win, acc);
+    if (a.nan) atomicAdd(&acc[2 * sc::kLimbs + sc::kNaN - 1], a.nan);
+    if (a.pinf) atomicAdd(&acc[2 * sc::kLimbs + sc::kPosInf - 1], a.pinf);
+    if (a.ninf) atomicAdd(&acc[2 * sc::kLimbs + sc::kNegInf - 1], a.ninf);
 }
 
 // A sum of non-negative terms (m2: dev*dev >= +0): one window, no sign test.
@@ -265,7 +331,7 @@ __global__ void finalize1_kernel(StageDev g) {
 struct P2Smem {
     unsigned long long acc[2 * sc::kAccWords];
     unsigned sel_all[sc::kB1];
-    unsigned sel_stop[sc::kB1];
+    unsigned sel_hz[sc::kB1];
     unsigned hist[kSmemHistBins];
 };
 
@@ -298,14 +364,14 @@ __global__ void __launch_bounds__(kPass2Threads, kPass2MinBlocks) pass2_kernel(c
     for (int i = threadIdx.x; i < 2 * sc::kAccWords; i += blockDim.x) S->acc[i] = 0ull;
     for (int i = threadIdx.x; i < sc::kB1; i += blockDim.x) {
         S->sel_all[i] = 0u;
-        S->sel_stop[i] = 0u;
+        S->sel_hz[i] = 0u;
     }
     if (hist_smem) {
         for (uint64_t i = threadIdx.x; i < s.bins; i += blockDim.x) S->hist[i] = 0u;
     }
     __syncthreads();
     RegAccPos m2;
-    RegAcc m3;
+    RegAccS m3;
     racc_init(m2);
     racc_init(m3);
     const double inv_bw = BMC_DIV(1.0, s.bin_width);
@@ -327,7 +393,7 @@ __global__ void __launch_bounds__(kPass2Threads, kPass2MinBlocks) pass2_kernel(c
         }
         const int b = sc::sel_bucket(v, s.sel_lo, s.sel_scale);
         atomicAdd(&S->sel_all[b], 1u);
-        if (!h) atomicAdd(&S->sel_stop[b], 1u);
+        if (h) atomicAdd(&S->sel_hz[b], 1u);  // rare: one atomic per result, not two
     };
     if (BMC_P2_VEC) {
         stream_results<true>(d, hz, n, [&](uint64_t, double v, unsigned h) { one(v, h != 0); });
@@ -356,10 +422,10 @@ __global__ void __launch_bounds__(kPass2Threads, kPass2MinBlocks) pass2_kernel(c
         if (S->acc[i]) atomicAdd(&p2[sc::kP2M2 + i], S->acc[i]);
     }
     const int sa = sc::p2_sel_all(g.summary ? g.hist_cap : 0);
-    const int ss = sc::p2_sel_stop(g.summary ? g.hist_cap : 0);
+    const int ss = sc::p2_sel_hz(g.summary ? g.hist_cap : 0);
     for (int i = threadIdx.x; i < sc::kB1; i += blockDim.x) {
         if (S->sel_all[i]) atomicAdd(&p2[sa + i], static_cast<unsigned long long>(S->sel_all[i]));
-        if (S->sel_stop[i]) atomicAdd(&p2[ss + i], static_cast<unsigned long long>(S->sel_stop[i]));
+        if (S->sel_hz[i]) atomicAdd(&p2[ss + i], static_cast<unsigned long long>(S->sel_hz[i]));
     }
     if (hist_smem) {
         for (uint64_t i = threadIdx.x; i < s.bins; i += blockDim.x) {
@@ -397,13 +463,15 @@ __global__ void __launch_bounds__(kTargetThreads) targets_kernel(StageDev g) {
     }
     __syncthreads();
     const unsigned long long* p2 = g.w + g.p2_sum;
-    const int off[2] = {sc::p2_sel_all(g.summary ? g.hist_cap : 0),
-                        sc::p2_sel_stop(g.summary ? g.hist_cap : 0)};
+    const int all = sc::p2_sel_all(g.summary ? g.hist_cap : 0);
+    const int hzo = sc::p2_sel_hz(g.summary ? g.hist_cap : 0);
     for (int pop = 0; pop < 2; ++pop) {
         unsigned long long items[kPer], sum = 0;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
-            items[k] = p2[off[pop] + threadIdx.x * kPer + k];
+            const int b = threadIdx.x * kPer + k;
+            // population 1 (stoppers) = all results - horizon hits, per bucket
+            items[k] = p2[all + b] - (pop ? p2[hzo + b] : 0ull);
             sum += items[k];
         }
         unsigned long long excl = 0;

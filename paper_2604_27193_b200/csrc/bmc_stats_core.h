@@ -247,8 +247,9 @@ constexpr int kP2M3 = kAccWords;       // exact sum of (d-mean)^3   (kAccWords)
 constexpr int kP2Hist = 2 * kAccWords; // summary histogram (hist_cap words)
 constexpr int kB1 = 4096;              // level-1 order-statistic buckets
 BMC_HD int p2_sel_all(uint64_t hist_cap) { return kP2Hist + static_cast<int>(hist_cap); }
-BMC_HD int p2_sel_stop(uint64_t hist_cap) { return p2_sel_all(hist_cap) + kB1; }
-BMC_HD int p2_sum_words(uint64_t hist_cap) { return p2_sel_stop(hist_cap) + kB1; }
+// level-1 counts of the horizon hits (rare): stoppers per bucket = all - hz
+BMC_HD int p2_sel_hz(uint64_t hist_cap) { return p2_sel_all(hist_cap) + kB1; }
+BMC_HD int p2_sum_words(uint64_t hist_cap) { return p2_sel_hz(hist_cap) + kB1; }
 
 // Scalars derived from the merged P1 (finalize_p1), stored as u64 words.
 struct Scalars {

@@ -70,7 +70,7 @@ struct HostBackend {
             if (hist_on) p2[sc::kP2Hist + sc::hist_index(v, s.lo, s.bin_width, s.bins)] += 1;
             const int b = sc::sel_bucket(v, s.sel_lo, s.sel_scale);
             p2[sc::p2_sel_all(hc) + b] += 1;
-            if (!h) p2[sc::p2_sel_stop(hc) + b] += 1;
+            if (h) p2[sc::p2_sel_hz(hc) + b] += 1;
         }
         ++launches;
         return BMC_OK;
@@ -93,15 +93,17 @@ struct HostBackend {
                 x.valid = x.rank >= 1 && x.rank <= s.stopped;
             }
             if (x.valid && x.rank) {
-                const uint64_t* h = p2 + (x.population ? sc::p2_sel_stop(hc) : sc::p2_sel_all(hc));
+                const uint64_t* all = p2 + sc::p2_sel_all(hc);
+                const uint64_t* hzb = p2 + sc::p2_sel_hz(hc);
                 uint64_t cum = 0;
                 for (int b = 0; b < sc::kB1; ++b) {
-                    if (cum + h[b] >= x.rank) {
+                    const uint64_t c = x.population ? all[b] - hzb[b] : all[b];  // stoppers
+                    if (cum + c >= x.rank) {
                         x.bucket = b;
                         x.residual = x.rank - cum;
                         break;
                     }
-                    cum += h[b];
+                    cum += c;
                 }
                 if (x.bucket < 0) x.valid = 0;
             }

@@ -369,3 +369,47 @@ def test_interleaved_worlds_never_rewrite_a_table_in_flight(ref, executor):
     torch.cuda.synchronize()
     assert np.array_equal(oa[0].cpu().numpy().view(np.uint64), want_a["stop_distance"].view(np.uint64))
     assert np.array_equal(ob[0].cpu().numpy().view(np.uint64), want_b["stop_distance"].view(np.uint64))
+
+
+_PIPE_DIGEST = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_2604_27193_b200 as bmc
+samples, _ = bmc.draw_batch(bmc.UncertaintyModel.mixed(23), 50000)
+ex = bmc.CudaExecutor(0)
+rep = ex.run(samples, chunk=6000)          # 9 chunks: three slots wrap three times
+r = rep.results
+h = hashlib.sha256()
+for f in ("stop_distance", "steps", "hit_horizon"):
+    h.update(np.ascontiguousarray(r[f]).tobytes())
+print(rep.chunks, rep.launches, h.hexdigest())
+"""
+
+
+def test_pipeline_output_paths_identical(ref):
+    """The streamed pipeline writes chunk outputs directly at each sample's
+    index (forward map); BMC_DIRECT_OUTPUTS=0 forces the packed-record +
+    unpermute path.  Both -- and the reference -- give the same bits.  (The
+    switch is read once per process, hence the subprocesses.)"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("1", "0"):
+        env = dict(os.environ, BMC_DIRECT_OUTPUTS=mode)
+        p = subprocess.run([sys.executable, "-c", _PIPE_DIGEST.format(root=root)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        chunks, launches, digest = p.stdout.split()[-3:]
+        outs[mode] = (int(chunks), int(launches), digest)
+    assert outs["1"][0] == outs["0"][0] == 9
+    # per chunk: predict, scan, scatter, rollout (+ unpermute on the packed path)
+    assert outs["1"][1] == 9 * 4 and outs["0"][1] == 9 * 5
+    assert outs["1"][2] == outs["0"][2]
+    samples, _ = ref.draw_batch(Model.mixed(23), 50000)
+    want, _, _ = ref.run(samples, World(), "parallel")
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(want["stop_distance"]).tobytes())
+    h.update(np.ascontiguousarray(want["steps"].astype(np.int64)).tobytes())
+    h.update(np.ascontiguousarray(want["hit_horizon"].astype(np.uint8)).tobytes())
+    assert outs["1"][2] == h.hexdigest()
