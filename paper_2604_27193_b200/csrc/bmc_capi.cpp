@@ -222,7 +222,8 @@ bool resolve_direct(int direct) {
     return direct == 1;
 }
 constexpr uint64_t kDirectChunkBytes = uint64_t{64} << 20;
-int pipeline_direct(uint64_t chunk) { return chunk * 13 <= kDirectChunkBytes ? 1 : 0; }
+
+int direct_outputs_for(uint64_t n) { return n * 13 <= kDirectChunkBytes ? 1 : 0; }
 
 int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n, int direct) {
     // counter: [0] work counter (u32) | [8] executed steps | [16] lane slots
@@ -432,7 +433,7 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
     }();
     const uint64_t nchunks = (n + chunk - 1) / chunk;
     const uint64_t used_slots = std::min(kSlots, nchunks);
-    const int direct = pipeline_direct(chunk);
+    const int direct = direct_outputs_for(chunk);
     for (uint64_t q = 0; q < used_slots; ++q) {
         Slot& s = ctx->slots[q];
         if (!dev_draw) BMC_CK(ctx, s.h_terms.reserve(chunk * 32));

@@ -226,6 +226,9 @@ int make_plan(bmc_ctx* ctx, const WorldDerived& d, const bmc_run_opts& opts, uin
 // unpermute; BMC_DIRECT_OUTPUTS=1 flips it), 0 = packed + unpermute,
 // 1 = direct writes at each sample's index through the forward map.
 int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n, int direct = -1);
+// 1 when a launch of n results writes them directly (13 B/result <= 64 MiB:
+// they merge in L2): the streamed pipeline's chunks and the decision graph.
+int direct_outputs_for(uint64_t n);
 // Device sampler (bmc_capi.cpp): resolve bmc_run_opts.sampler to a yes/no.
 int use_device_sampler(bmc_ctx* ctx, const bmc_run_opts& o, bool* device);
 // Fill DrawArgs from a model + world (no output pointers set).

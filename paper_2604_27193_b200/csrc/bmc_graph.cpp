@@ -127,7 +127,8 @@ bool capture_rollout_tail(bmc_graph* g, const bmc_terms& terms, const bmc_output
         if (bmc::stats_begin_enqueue(g->st, s) != BMC_OK) return false;
     }
     if (bmc::enqueue_rollout(ctx, g->plan, g->sc, terms, n, outs, g->steps_total.as<unsigned long long>(),
-                             s, nullptr, launches, g->st ? &p1 : nullptr) != BMC_OK) {
+                             s, nullptr, launches, g->st ? &p1 : nullptr,
+                             bmc::direct_outputs_for(n)) != BMC_OK) {
         return false;
     }
     if (g->st) {
@@ -242,7 +243,7 @@ int graph_create(bmc_ctx* ctx, size_t n, const bmc_world* world, const bmc_run_o
     BMC_CK(ctx, g->d_terms.reserve(n * 32));
     BMC_CK(ctx, g->d_out.reserve(n * 13));
     BMC_CK(ctx, g->steps_total.reserve(sizeof(unsigned long long)));
-    if ((rc = bmc::reserve_scratch(ctx, g->sc, g->plan, n)) != BMC_OK) return rc;
+    if ((rc = bmc::reserve_scratch(ctx, g->sc, g->plan, n, bmc::direct_outputs_for(n))) != BMC_OK) return rc;
     BMC_CK(ctx, cudaEventCreateWithFlags(&g->done, cudaEventDisableTiming));
     BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
 
