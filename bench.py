@@ -204,9 +204,14 @@ def cpu_baseline(args, n_total):
     n = int(min(n_total, max(2000, args.cpu_seconds * 2000.0 / t_probe)))
     samples, _ = ref.draw_batch(model, n)
     _, wall, wc = ref.run(samples, World(), "parallel", 0)
+    # the reference's single-core executor too (run_sequential, backends.cpp:38-55)
+    ns = min(n, 10000)
+    _, wall_s, _ = ref.run(samples[:ns], World(), "sequential")
     return {"value": n / wall, "unit": "rollouts/s", "cores": wc, "kind": "reference",
             "sample": f"{n} samples (prefix of the seed-{args.seed} batch), reference "
-                      f"run_parallel with {wc} threads, {wall:.1f} s"}
+                      f"run_parallel with {wc} threads, {wall:.1f} s",
+            "sequential": {"value": ns / wall_s, "unit": "rollouts/s", "cores": 1,
+                           "sample": f"{ns} samples, reference run_sequential, {wall_s:.1f} s"}}
 
 
 # -------------------------------------------------------------------- b200
