@@ -232,7 +232,7 @@ int reserve_scratch(bmc_ctx* ctx, Scratch& sc, const Plan& plan, uint64_t n, int
         const uint64_t m = std::max<uint64_t>(n, 1);
         BMC_CK(ctx, sc.keys.reserve(m * sizeof(uint16_t)));
         BMC_CK(ctx, sc.perm.reserve(m * sizeof(uint32_t)));  // forward (or inverse) permutation
-        BMC_CK(ctx, sc.hist.reserve(4096 * sizeof(unsigned int)));
+        BMC_CK(ctx, sc.hist.reserve(bin_windows(m) * 4096 * sizeof(unsigned int)));
         BMC_CK(ctx, sc.packed_in.reserve(m * sizeof(PackedTerms)));
         if (!resolve_direct(direct)) BMC_CK(ctx, sc.packed_out.reserve(m * sizeof(PackedOut)));
     }
@@ -257,7 +257,7 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
     if (plan.sched == kScheduleBinned && n > 0) {
         const int buckets = bucket_count(d);
         if (ev) BMC_CK(ctx, cudaEventRecord(ev->p0, s));
-        BMC_CK(ctx, cudaMemsetAsync(sc.hist.p, 0, buckets * sizeof(unsigned int), s));
+        BMC_CK(ctx, cudaMemsetAsync(sc.hist.p, 0, bin_windows(n) * buckets * sizeof(unsigned int), s));
         PredictArgs pa{};
         pa.v0 = terms.initial_speed;
         pa.brake_floor = terms.brake_floor;
@@ -277,11 +277,11 @@ int enqueue_rollout(bmc_ctx* ctx, const Plan& plan, Scratch& sc, const bmc_terms
         pa.keys = sc.keys.as<uint16_t>();
         pa.hist = sc.hist.as<unsigned int>();
         BMC_CK(ctx, launch_predict(pa, s));
-        BMC_CK(ctx, launch_bin_scan(sc.hist.as<unsigned int>(), buckets, s));
+        BMC_CK(ctx, launch_bin_scan(sc.hist.as<unsigned int>(), buckets, n, s));
         BMC_CK(ctx, launch_bin_scatter(sc.keys.as<uint16_t>(), n, sc.hist.as<unsigned int>(),
                                        terms.initial_speed, terms.brake_floor, terms.drag_factor,
                                        terms.grade_accel, sc.packed_in.as<PackedTerms>(),
-                                       sc.perm.as<uint32_t>(), direct_out ? 1 : 0, s));
+                                       sc.perm.as<uint32_t>(), direct_out ? 1 : 0, buckets, s));
         if (ev) BMC_CK(ctx, cudaEventRecord(ev->p1, s));
         nl += 3;
         packed = true;

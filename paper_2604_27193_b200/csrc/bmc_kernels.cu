@@ -655,8 +655,13 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictArgs P) {
     const float h = P.h, hh = 0.5f * P.h, h6 = P.h / 6.0f;
     const int ks = P.coarse_steps;  // <= (coarse_len - 1) / 2
     const float t_s = static_cast<float>(ks) * h;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P.n;
+    // blocks [w * bpw, (w + 1) * bpw) cover binning window w
+    const unsigned bpw = gridDim.x / static_cast<unsigned>(bin_windows(P.n));
+    const uint64_t w = blockIdx.x / bpw;
+    const uint64_t lo = w << kBinWindowLog2;
+    const uint64_t hi = min(P.n, lo + (uint64_t{1} << kBinWindowLog2));
+    const uint64_t stride = static_cast<uint64_t>(bpw) * blockDim.x;
+    for (uint64_t i = lo + static_cast<uint64_t>(blockIdx.x % bpw) * blockDim.x + threadIdx.x; i < hi;
          i += stride) {
         float v = static_cast<float>(P.v0[i]);
         const float F = static_cast<float>(P.brake_floor[i]);
@@ -695,23 +700,30 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictArgs P) {
         int pred = P.max_steps;
         if (tstar >= 0.0f) pred = static_cast<int>(fminf(ceilf(tstar * P.inv_dt), 2e9f));
         pred = max(1, min(pred, P.max_steps));
-        // key = (descending step bucket, clamp class): warps see one class,
-        // so the never-clamping majority runs the select-free loop body
+        // key = (clamp class, descending step bucket), class-major: warps see
+        // one class, so the never-clamping majority runs the select-free loop
+        // body.  Class-major because the sort is per binning window: with
+        // step-major keys every window had hundreds of class boundaries, and
+        // a warp straddling one ran the select + per-step-test band up to the
+        // table head (+2.7% instructions, 96.2% FP64 pipe, ncu)
         const int sb = (P.max_steps - pred) / P.bucket_width;
         const int cls = P.brake_floor[i] < P.table_min ? 0 : 1;
-        const int bucket = min(2 * sb + cls, P.buckets - 1);
+        const int bucket = min(cls * (P.buckets >> 1) + sb, P.buckets - 1);
         P.keys[i] = static_cast<uint16_t>(bucket);
         atomicAdd(&s_hist[bucket], 1u);
     }
     __syncthreads();
     for (int b = threadIdx.x; b < P.buckets; b += blockDim.x) {
         const unsigned int c = s_hist[b];
-        if (c) atomicAdd(&P.hist[b], c);
+        if (c) atomicAdd(&P.hist[w * P.buckets + b], c);
     }
 }
 
-__global__ void __launch_bounds__(1024) bin_scan_kernel(unsigned int* hist, int buckets) {
-    // exclusive scan, in place: counts -> start cursor of each bucket
+__global__ void __launch_bounds__(1024) bin_scan_kernel(unsigned int* hist_all, int buckets) {
+    // exclusive scan, in place: counts -> start cursor of each bucket; block
+    // w scans window w, whose sorted slots start at w * 2^20 (full windows)
+    unsigned int* hist = hist_all + static_cast<size_t>(blockIdx.x) * buckets;
+    const unsigned int base = static_cast<unsigned int>(blockIdx.x) << kBinWindowLog2;
     using Scan = cub::BlockScan<unsigned int, 1024>;
     __shared__ typename Scan::TempStorage tmp;
     constexpr int kPer = kMaxBuckets / 1024;
@@ -723,7 +735,7 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(unsigned int* hist, int 
     Scan(tmp).ExclusiveSum(items, items);
     for (int k = 0; k < kPer; ++k) {
         const int b = threadIdx.x * kPer + k;
-        if (b < buckets) hist[b] = items[k];
+        if (b < buckets) hist[b] = base + items[k];
     }
 }
 
@@ -734,7 +746,7 @@ template <int kItems>
 __global__ void __launch_bounds__(256, BMC_SCATTER_PRELOAD ? 2 : 1)
     bin_scatter_kernel(const uint16_t* keys, uint64_t n, unsigned int* cursor, const double* v0,
                        const double* floor_, const double* drag, const double* grade,
-                       PackedTerms* packed, uint32_t* perm, int forward) {
+                       PackedTerms* packed, uint32_t* perm, int forward, int buckets) {
     // Tile-aggregated counting-sort scatter: ranks inside a 2048-sample tile
     // come from shared-memory atomics; each (tile, bucket) reserves its slots
     // with ONE global atomic, so hot buckets are not serialised per warp.
@@ -771,9 +783,11 @@ __global__ void __launch_bounds__(256, BMC_SCATTER_PRELOAD ? 2 : 1)
             if (i < n) rank[k] = atomicAdd(&s_cnt[key[k]], 1u);
         }
         __syncthreads();
+        // a tile lies inside one binning window (2^20 is a multiple of kTile)
+        unsigned int* wcur = cursor + (tile >> kBinWindowLog2) * static_cast<uint64_t>(buckets);
         for (int b = threadIdx.x; b < kMaxBuckets; b += 256) {
             const unsigned c = s_cnt[b];
-            if (c) s_base[b] = atomicAdd(&cursor[b], c);
+            if (c) s_base[b] = atomicAdd(&wcur[b], c);
         }
         __syncthreads();
 #pragma unroll
@@ -802,7 +816,7 @@ __global__ void __launch_bounds__(256, BMC_SCATTER_PRELOAD ? 2 : 1)
 }
 
 #ifndef BMC_UNPERMUTE_ILP
-#define BMC_UNPERMUTE_ILP 4
+#define BMC_UNPERMUTE_ILP 8
 #endif
 // Index-order gather of the packed sorted outputs: kUnp independent
 // (slot -> record) gathers in flight per thread (one at a time left the
@@ -967,23 +981,27 @@ cudaError_t launch_predict(const PredictArgs& a, cudaStream_t s) {
     if (a.buckets > kMaxBuckets || a.buckets < 1) return cudaErrorInvalidValue;
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint64_t blocks_needed = (a.n + 255) / 256;
-    const int grid = static_cast<int>(std::min<uint64_t>(blocks_needed,
-                                                         static_cast<uint64_t>(sm_count(dev)) * 8));
+    // bpw blocks per binning window, ~8 CTAs per SM in all
+    const uint64_t nwin = bin_windows(a.n);
+    const uint64_t target = static_cast<uint64_t>(sm_count_cached(dev)) * 8;
+    const uint64_t per_win = std::min<uint64_t>(uint64_t{1} << kBinWindowLog2, a.n);
+    const uint64_t bpw = std::max<uint64_t>(1, std::min<uint64_t>((per_win + 255) / 256,
+                                                                  (target + nwin - 1) / nwin));
+    const int grid = static_cast<int>(nwin * bpw);
     predict_kernel<<<grid, 256, static_cast<size_t>(a.coarse_len) * sizeof(float), s>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t launch_bin_scan(unsigned int* hist, int buckets, cudaStream_t s) {
+cudaError_t launch_bin_scan(unsigned int* hist, int buckets, uint64_t n, cudaStream_t s) {
     if (buckets > kMaxBuckets) return cudaErrorInvalidValue;
-    bin_scan_kernel<<<1, 1024, 0, s>>>(hist, buckets);
+    bin_scan_kernel<<<static_cast<int>(std::max<uint64_t>(1, bin_windows(n))), 1024, 0, s>>>(hist, buckets);
     return cudaGetLastError();
 }
 
 cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* cursor,
                                const double* v0, const double* brake_floor, const double* drag,
                                const double* grade, PackedTerms* packed, uint32_t* perm,
-                               int forward, cudaStream_t s) {
+                               int forward, int buckets, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     // 8 items per thread (2048-sample tiles); 16 and 32 were measured slower
@@ -993,7 +1011,7 @@ cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* c
     const int grid = static_cast<int>(std::min<uint64_t>(blocks_needed,
                                                          static_cast<uint64_t>(sm_count_cached(dev)) * 8));
     bin_scatter_kernel<8><<<grid, 256, 0, s>>>(keys, n, cursor, v0, brake_floor, drag, grade, packed,
-                                               perm, forward);
+                                               perm, forward, buckets);
     return cudaGetLastError();
 }
 

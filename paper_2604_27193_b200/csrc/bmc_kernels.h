@@ -70,8 +70,22 @@ struct PredictArgs {
     int32_t buckets;        // total keys = 2 * step buckets (clamp class bit)
     double table_min;       // min actuator stage value: F < table_min never clamps
     uint16_t* keys;         // out: bucket per sample (descending predicted steps)
-    unsigned int* hist;     // out: per-bucket counts (zeroed before launch)
+    unsigned int* hist;     // out: per-(window, bucket) counts (zeroed before launch)
 };
+
+// Binning windows: samples are sorted within consecutive index windows of
+// 2^kBinWindowLog2 (window-major sorted order).  Smaller windows keep the
+// counting-sort scatter's writes local (2^20: scatter 4.45 -> 2.0 ms at 1e8)
+// but cost the rollout more than that (921.6 vs 916.4 ms with 2^20 / one
+// window; 2^22: 919.2 ms), so the windows are 2^27 samples: one window up
+// to 1.3e8 (profiles/round2_hbm_stage_ab.txt, section E).
+constexpr int kBinWindowLog2 = 27;
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline uint64_t bin_windows(uint64_t n) {
+    return (n + (uint64_t{1} << kBinWindowLog2) - 1) >> kBinWindowLog2;
+}
 
 // On-device sampler (bmc_sampler.cu): samples [first, first+n) of
 // draw_batch(model, .) and their RolloutTerms, bit-identical to the host
@@ -135,7 +149,7 @@ cudaError_t launch_rollout(const RolloutArgs& a, int table_mode, int block_threa
                            int unroll, cudaStream_t s);
 cudaError_t launch_predict(const PredictArgs& a, cudaStream_t s);
 cudaError_t launch_fp64_probe(double* out, int iters, uint64_t* ops, cudaStream_t s);
-cudaError_t launch_bin_scan(unsigned int* hist_to_cursor, int buckets, cudaStream_t s);
+cudaError_t launch_bin_scan(unsigned int* hist_to_cursor, int buckets, uint64_t n, cudaStream_t s);
 // counting-sort scatter: inv_perm[i] = sorted slot of sample i, and the
 // sample's inputs are written packed into that slot
 // forward != 0: perm[slot] = i (sorted slot -> sample, for direct SoA
@@ -143,7 +157,7 @@ cudaError_t launch_bin_scan(unsigned int* hist_to_cursor, int buckets, cudaStrea
 cudaError_t launch_bin_scatter(const uint16_t* keys, uint64_t n, unsigned int* cursor,
                                const double* v0, const double* brake_floor, const double* drag,
                                const double* grade, PackedTerms* packed, uint32_t* perm,
-                               int forward, cudaStream_t s);
+                               int forward, int buckets, cudaStream_t s);
 // outputs back to index order: out[j] = packed_out[inv_perm[j]]
 cudaError_t launch_unpermute(const PackedOut* packed_out, const uint32_t* inv_perm, uint64_t n,
                              double* stop_distance, int32_t* steps, uint8_t* hit_horizon,
