@@ -816,12 +816,13 @@ __global__ void __launch_bounds__(256, BMC_SCATTER_PRELOAD ? 2 : 1)
 }
 
 #ifndef BMC_UNPERMUTE_ILP
-#define BMC_UNPERMUTE_ILP 8
+#define BMC_UNPERMUTE_ILP 4
 #endif
 // Index-order gather of the packed sorted outputs: kUnp independent
-// (slot -> record) gathers in flight per thread (one at a time left the
-// kernel latency-bound at 2.3% issue, ncu); the 16-B records sit at random
-// slots, so each costs a full 32-B sector (74 B/sample DRAM for 33 algorithmic).
+// (slot -> record) gathers in flight per thread, one 16-B load each; the
+// records sit at random slots, so each costs a full 32-B sector (73 B/sample
+// DRAM for 33 algorithmic).  8 in flight: 2.47 ms but 123 B/sample of DRAM
+// reads; 4: 2.66 ms at 73 B/sample (ncu, profiles/round2_hbm_stage_ab.txt).
 __global__ void __launch_bounds__(256) unpermute_kernel(const PackedOut* packed_out,
                                                         const uint32_t* inv_perm, uint64_t n,
                                                         double* d, int32_t* steps, uint8_t* hz) {

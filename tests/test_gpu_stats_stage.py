@@ -230,7 +230,7 @@ def test_two_ranks_on_one_gpu_merge_bitwise(ref):
 
 
 def test_run_model_stream_with_fused_statistics(ref, executor):
-    """bmc_cuda_run_model_stats: pass 1 in every chunk's rollout (both slot
+    """bmc_cuda_run_model_stats: pass 1 in every chunk's rollout (every slot
     streams), the rest after the stream -- equal to the one-call stage."""
     import torch
     m = Model.mixed(19)
