@@ -375,6 +375,10 @@ __global__ void __launch_bounds__(kPass2Threads, kPass2MinBlocks) pass2_kernel(c
     racc_init(m2);
     racc_init(m3);
     const double inv_bw = BMC_DIV(1.0, s.bin_width);
+    // a power-of-two bin width (the reference's default 2 m): d / bw == d * (1 / bw)
+    // exactly (both are the correctly rounded scaling by 2^-k), no margin test
+    const bool bw_pow2 = (sc::bits_of(s.bin_width) & 0x000FFFFFFFFFFFFFull) == 0 &&
+                         s.bin_width > 0.0 && inv_bw < 1.0 / 0.0 && inv_bw > 0.0;
     auto one = [&](double v, bool h) {
         if (summary) {
             const double dev = BMC_SUB(v, s.mean);
@@ -384,7 +388,15 @@ __global__ void __launch_bounds__(kPass2Threads, kPass2MinBlocks) pass2_kernel(c
         }
         if (sc::is_nan(v)) return;
         if (hist_on) {
-            const uint64_t idx = sc::hist_index_fast(v, s.lo, s.bin_width, inv_bw, s.bins);
+            uint64_t idx;
+            if (bw_pow2) {
+                const double q = BMC_MUL(BMC_SUB(v, s.lo), inv_bw);
+                idx = !(q < 18446744073709551616.0) ? s.bins - 1
+                      : (!(q >= 0.0) ? 0 : static_cast<uint64_t>(q));
+                idx = idx >= s.bins ? s.bins - 1 : idx;
+            } else {
+                idx = sc::hist_index_fast(v, s.lo, s.bin_width, inv_bw, s.bins);
+            }
             if (hist_smem) {
                 atomicAdd(&S->hist[idx], 1u);
             } else {

@@ -335,6 +335,13 @@ int stats_compose(B& be, const StatsConfig& cfg, const StatsLayout& L, StatsRead
         return BMC_E_CONFIG;
     }
     if (cfg.summary && s.hist_overflow) {
+        // the reference sizes counts with (size_t)ceil((hi - lo) / bw) (analysis.cpp:61-63):
+        // a non-finite or extreme range has no usable histogram there either
+        if (s.bins > (uint64_t{1} << 30)) {
+            *err = "summarize: histogram of " + std::to_string(s.bins) +
+                   " bins (non-finite or extreme stop-distance range)";
+            return BMC_E_RANGE;
+        }
         rb.hist.assign(s.bins, 0);
         if ((rc = be.hist_full(d, n, s.lo, s.bin_width, s.bins, rb.hist.data())) != BMC_OK) return rc;
         if (merging) {

@@ -250,3 +250,49 @@ def test_run_model_stream_with_fused_statistics(ref, executor):
     _same(got, host_stats(want["stop_distance"], want["hit_horizon"], req))
     check_vs_reference(ref, want, got, req)
     stage.close()
+
+
+def _pass2_batch(kind):
+    """Data aimed at pass 2's paths: the 128-bit fixed-point sums (terms on
+    the grid), their superaccumulator fallback (values within a few ulps of
+    the batch mean, so dev*dev lies far below the grid), both signs of m3
+    terms, zero deviations, bin edges and their neighbours for the
+    power-of-two histogram index, and non-finite values that switch the fast
+    path off."""
+    rng = np.random.default_rng(11)
+    x = np.round(rng.normal(0.0, 12.0, 150000) * 2.0 ** 20) / 2.0 ** 20
+    edges = np.arange(20.0, 140.0, 0.5)
+    base = np.concatenate([80.0 + x, 80.0 - x, edges, np.nextafter(edges, 0.0), [900.0, -150.0]])
+    m = math.fsum(base) / base.size          # the batch mean (pairs about it keep it)
+    k = np.arange(1, 200) * np.spacing(m)
+    d = np.concatenate([base, np.full(3000, m), m + k, m - k])
+    if kind == "nan":
+        d = np.concatenate([d, [np.nan] * 5])
+    elif kind == "inf":
+        d = np.concatenate([d, [np.inf, 3.0]])
+    rng.shuffle(d)
+    hz = (rng.random(d.shape[0]) < 0.01).astype(np.uint8)
+    return d, hz
+
+
+@pytest.mark.parametrize("kind", ["finite", "nan", "inf"])
+@pytest.mark.parametrize("bw", [2.0, 0.5, 0.37])
+def test_device_pass2_fast_paths_exact(ref, executor, kind, bw):
+    d, hz = _pass2_batch(kind)
+    res = _mk(d, hz)
+    req = StatsRequest(headways=[50.0, 80.0, 100.0], risk_levels=RISKS, summarize=True,
+                       bin_width=bw)
+    dd, hh = _dev(res)
+    if kind == "inf":
+        # +inf makes the reference's bin count (size_t)ceil(inf / bw) undefined: both the
+        # device stage and its host twin refuse with BMC_E_RANGE instead of allocating
+        with pytest.raises(bmc.BmcError) as e_dev:
+            executor.stats(dd, hh, req.headways, req.risk_levels, True, bw)
+        with pytest.raises(bmc.BmcError) as e_host:
+            host_stats(res["stop_distance"], res["hit_horizon"], req)
+        assert e_dev.value.code == e_host.value.code == -5 and "bins" in str(e_dev.value)
+        return
+    got = executor.stats(dd, hh, req.headways, req.risk_levels, True, bw)
+    _same(got, host_stats(res["stop_distance"], res["hit_horizon"], req))
+    if kind == "finite":
+        check_vs_reference(ref, res, got, req)

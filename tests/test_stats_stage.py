@@ -251,3 +251,14 @@ def test_gloo_merge_equals_single_rank_bitwise(ref, world, cand_cap):
         assert o["out"] == _jsonable(single)
     # three merge points: P1 (SUM + MIN), P2 (SUM), candidates (counts + keys)
     assert outs[0]["calls"] >= 5
+
+
+def test_infinite_range_histogram_refused():
+    """+inf stop distances make the reference's bin count (size_t)ceil(inf / bw)
+    undefined (analysis.cpp:61-63); the stage refuses with BMC_E_RANGE rather
+    than sizing a 2^64-bin histogram."""
+    from paper_2604_27193_b200 import BmcError
+    req = StatsRequest(headways=[1.0], risk_levels=[0.05], summarize=True, bin_width=2.0)
+    with pytest.raises(BmcError) as e:
+        host_stats(np.array([1.0, 2.0, np.inf]), None, req)
+    assert e.value.code == -5 and "bins" in str(e.value)
