@@ -647,59 +647,67 @@ using bmc::fail;
 extern "C" {
 
 int bmc_device_count(int* out) {
-    int c = 0;
-    const cudaError_t e = cudaGetDeviceCount(&c);
-    if (e != cudaSuccess) {
-        *out = 0;
-        return fail(nullptr, BMC_E_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    try {
+        int c = 0;
+        const cudaError_t e = cudaGetDeviceCount(&c);
+        if (e != cudaSuccess) {
+            *out = 0;
+            return fail(nullptr, BMC_E_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+        }
+        *out = c;
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception();
     }
-    *out = c;
-    return BMC_OK;
 }
 
 int bmc_cuda_init(int device, bmc_ctx** out) {
-    if (out == nullptr) return fail(nullptr, BMC_E_CONFIG, "bmc_cuda_init: null output");
-    *out = nullptr;
-    int count = 0;
-    cudaError_t e = cudaGetDeviceCount(&count);
-    if (e != cudaSuccess || count == 0) {
-        return fail(nullptr, BMC_E_CUDA,
-                    std::string("no CUDA device: ") + (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
-    }
-    if (device < 0 || device >= count) {
-        return fail(nullptr, BMC_E_CONFIG, "execution.device: out of range");
-    }
-    cudaDeviceProp prop{};
-    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) {
-        return fail(nullptr, BMC_E_CUDA, std::string("cudaGetDeviceProperties: ") + cudaGetErrorString(e));
-    }
-    if (prop.major != 10) {
-        return fail(nullptr, BMC_E_CUDA,
-                    "device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
-                        "; this build targets sm_100a only");
-    }
-    auto ctx = std::make_unique<bmc_ctx>();
-    ctx->device = device;
-    ctx->sms = prop.multiProcessorCount;
-    if ((e = cudaSetDevice(device)) != cudaSuccess ||
-        (e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess ||
-        (e = cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking)) != cudaSuccess ||
-        (e = cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking)) != cudaSuccess ||
-        (e = ctx->kev.create()) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&ctx->scratch_done, cudaEventDisableTiming)) != cudaSuccess) {
-        return fail(nullptr, BMC_E_CUDA, std::string("context setup: ") + cudaGetErrorString(e));
-    }
-    for (auto& s : ctx->slots) {
-        if ((e = cudaStreamCreateWithFlags(&s.compute, cudaStreamNonBlocking)) != cudaSuccess ||
-            (e = cudaEventCreateWithFlags(&s.h2d_done, cudaEventDisableTiming)) != cudaSuccess ||
-            (e = cudaEventCreateWithFlags(&s.compute_done, cudaEventDisableTiming)) != cudaSuccess ||
-            (e = cudaEventCreateWithFlags(&s.d2h_done, cudaEventDisableTiming)) != cudaSuccess ||
-            (e = s.kev.create()) != cudaSuccess) {
-            return fail(nullptr, BMC_E_CUDA, std::string("context events: ") + cudaGetErrorString(e));
+    try {
+        if (out == nullptr) return fail(nullptr, BMC_E_CONFIG, "bmc_cuda_init: null output");
+        *out = nullptr;
+        int count = 0;
+        cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0) {
+            return fail(nullptr, BMC_E_CUDA,
+                        std::string("no CUDA device: ") + (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
         }
+        if (device < 0 || device >= count) {
+            return fail(nullptr, BMC_E_CONFIG, "execution.device: out of range");
+        }
+        cudaDeviceProp prop{};
+        if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) {
+            return fail(nullptr, BMC_E_CUDA, std::string("cudaGetDeviceProperties: ") + cudaGetErrorString(e));
+        }
+        if (prop.major != 10) {
+            return fail(nullptr, BMC_E_CUDA,
+                        "device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
+                            "; this build targets sm_100a only");
+        }
+        auto ctx = std::make_unique<bmc_ctx>();
+        ctx->device = device;
+        ctx->sms = prop.multiProcessorCount;
+        if ((e = cudaSetDevice(device)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = ctx->kev.create()) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&ctx->scratch_done, cudaEventDisableTiming)) != cudaSuccess) {
+            return fail(nullptr, BMC_E_CUDA, std::string("context setup: ") + cudaGetErrorString(e));
+        }
+        for (auto& s : ctx->slots) {
+            if ((e = cudaStreamCreateWithFlags(&s.compute, cudaStreamNonBlocking)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&s.h2d_done, cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&s.compute_done, cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&s.d2h_done, cudaEventDisableTiming)) != cudaSuccess ||
+                (e = s.kev.create()) != cudaSuccess) {
+                return fail(nullptr, BMC_E_CUDA, std::string("context events: ") + cudaGetErrorString(e));
+            }
+        }
+        *out = ctx.release();
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception();
     }
-    *out = ctx.release();
-    return BMC_OK;
 }
 
 void bmc_cuda_destroy(bmc_ctx* ctx) {
@@ -741,203 +749,263 @@ const char* bmc_cuda_last_error(const bmc_ctx* ctx) { return ctx ? ctx->err.c_st
 void* bmc_cuda_stream(bmc_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
 int bmc_cuda_sync(bmc_ctx* ctx) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
-    return BMC_OK;
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_rollout_device(bmc_ctx* ctx, const bmc_terms* terms, size_t n, const bmc_world* world,
                             const bmc_run_opts* opts, const bmc_outputs* out,
                             unsigned long long* total_steps_dev, void* stream) {
-    return bmc_cuda_rollout_stats(ctx, terms, n, world, opts, out, total_steps_dev, nullptr, stream);
+    try {
+        return bmc_cuda_rollout_stats(ctx, terms, n, world, opts, out, total_steps_dev, nullptr, stream);
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_last_kernel_ms(bmc_ctx* ctx, float* rollout_ms, float* predict_ms) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    float r = 0.0f, p = 0.0f;
-    BMC_CK(ctx, cudaEventSynchronize(ctx->kev.r1));
-    BMC_CK(ctx, cudaEventElapsedTime(&r, ctx->kev.r0, ctx->kev.r1));
-    if (ctx->kev.predicted) BMC_CK(ctx, cudaEventElapsedTime(&p, ctx->kev.p0, ctx->kev.p1));
-    if (rollout_ms) *rollout_ms = r;
-    if (predict_ms) *predict_ms = p;
-    return BMC_OK;
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        float r = 0.0f, p = 0.0f;
+        BMC_CK(ctx, cudaEventSynchronize(ctx->kev.r1));
+        BMC_CK(ctx, cudaEventElapsedTime(&r, ctx->kev.r0, ctx->kev.r1));
+        if (ctx->kev.predicted) BMC_CK(ctx, cudaEventElapsedTime(&p, ctx->kev.p0, ctx->kev.p1));
+        if (rollout_ms) *rollout_ms = r;
+        if (predict_ms) *predict_ms = p;
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_last_stage_ms(bmc_ctx* ctx, float* bin_ms, float* rollout_ms, float* unpermute_ms) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    float b = 0.0f, r = 0.0f, u = 0.0f;
-    BMC_CK(ctx, cudaEventSynchronize(ctx->kev.r1));
-    BMC_CK(ctx, cudaEventElapsedTime(&r, ctx->kev.r0, ctx->kev.r1));
-    if (ctx->kev.predicted) BMC_CK(ctx, cudaEventElapsedTime(&b, ctx->kev.p0, ctx->kev.p1));
-    if (ctx->kev.unpermuted) {
-        BMC_CK(ctx, cudaEventSynchronize(ctx->kev.u1));
-        BMC_CK(ctx, cudaEventElapsedTime(&u, ctx->kev.r1, ctx->kev.u1));
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        float b = 0.0f, r = 0.0f, u = 0.0f;
+        BMC_CK(ctx, cudaEventSynchronize(ctx->kev.r1));
+        BMC_CK(ctx, cudaEventElapsedTime(&r, ctx->kev.r0, ctx->kev.r1));
+        if (ctx->kev.predicted) BMC_CK(ctx, cudaEventElapsedTime(&b, ctx->kev.p0, ctx->kev.p1));
+        if (ctx->kev.unpermuted) {
+            BMC_CK(ctx, cudaEventSynchronize(ctx->kev.u1));
+            BMC_CK(ctx, cudaEventElapsedTime(&u, ctx->kev.r1, ctx->kev.u1));
+        }
+        if (bin_ms) *bin_ms = b;
+        if (rollout_ms) *rollout_ms = r;
+        if (unpermute_ms) *unpermute_ms = u;
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    if (bin_ms) *bin_ms = b;
-    if (rollout_ms) *rollout_ms = r;
-    if (unpermute_ms) *unpermute_ms = u;
-    return BMC_OK;
 }
 
 int bmc_cuda_last_lane_stats(bmc_ctx* ctx, uint64_t* steps, uint64_t* slots) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    unsigned long long c[2] = {0, 0};
-    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
-    if (ctx->scratch.counter.p) {
-        BMC_CK(ctx, cudaMemcpy(c, ctx->scratch.counter.as<char>() + 8, sizeof c, cudaMemcpyDeviceToHost));
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        unsigned long long c[2] = {0, 0};
+        BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
+        if (ctx->scratch.counter.p) {
+            BMC_CK(ctx, cudaMemcpy(c, ctx->scratch.counter.as<char>() + 8, sizeof c, cudaMemcpyDeviceToHost));
+        }
+        if (steps) *steps = c[0];
+        if (slots) *slots = c[1];
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    if (steps) *steps = c[0];
-    if (slots) *slots = c[1];
-    return BMC_OK;
 }
 
 int bmc_cuda_fp64_peak(bmc_ctx* ctx, int reps, double* ops_per_s, double* best_ms) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    BMC_CK(ctx, ctx->scratch.counter.reserve(64));
-    double best = 1e30;
-    uint64_t ops = 0;
-    for (int r = 0; r < std::max(1, reps) + 1; ++r) {  // first launch is a warm-up
-        BMC_CK(ctx, cudaEventRecord(ctx->kev.r0, ctx->stream));
-        BMC_CK(ctx, bmc::launch_fp64_probe(ctx->scratch.counter.as<double>(), 4096, &ops, ctx->stream));
-        BMC_CK(ctx, cudaEventRecord(ctx->kev.r1, ctx->stream));
-        BMC_CK(ctx, cudaEventSynchronize(ctx->kev.r1));
-        float ms = 0.0f;
-        BMC_CK(ctx, cudaEventElapsedTime(&ms, ctx->kev.r0, ctx->kev.r1));
-        if (r > 0) best = std::min(best, static_cast<double>(ms));
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        BMC_CK(ctx, ctx->scratch.counter.reserve(64));
+        double best = 1e30;
+        uint64_t ops = 0;
+        for (int r = 0; r < std::max(1, reps) + 1; ++r) {  // first launch is a warm-up
+            BMC_CK(ctx, cudaEventRecord(ctx->kev.r0, ctx->stream));
+            BMC_CK(ctx, bmc::launch_fp64_probe(ctx->scratch.counter.as<double>(), 4096, &ops, ctx->stream));
+            BMC_CK(ctx, cudaEventRecord(ctx->kev.r1, ctx->stream));
+            BMC_CK(ctx, cudaEventSynchronize(ctx->kev.r1));
+            float ms = 0.0f;
+            BMC_CK(ctx, cudaEventElapsedTime(&ms, ctx->kev.r0, ctx->kev.r1));
+            if (r > 0) best = std::min(best, static_cast<double>(ms));
+        }
+        if (ops_per_s) *ops_per_s = static_cast<double>(ops) / (best * 1e-3);
+        if (best_ms) *best_ms = best;
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    if (ops_per_s) *ops_per_s = static_cast<double>(ops) / (best * 1e-3);
-    if (best_ms) *best_ms = best;
-    return BMC_OK;
 }
 
 int bmc_cuda_alloc(bmc_ctx* ctx, size_t bytes, void** out) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    if (!out) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_alloc: null output");
-    *out = nullptr;
-    const cudaError_t e = cudaMalloc(out, bytes ? bytes : 1);
-    if (e != cudaSuccess) return fail(ctx, BMC_E_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    return BMC_OK;
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        if (!out) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_alloc: null output");
+        *out = nullptr;
+        const cudaError_t e = cudaMalloc(out, bytes ? bytes : 1);
+        if (e != cudaSuccess) return fail(ctx, BMC_E_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_free(bmc_ctx* ctx, void* ptr) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    if (ptr) BMC_CK(ctx, cudaFree(ptr));
-    return BMC_OK;
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        if (ptr) BMC_CK(ctx, cudaFree(ptr));
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_copy_to_host(bmc_ctx* ctx, void* host, const void* dev, size_t bytes) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if (bytes == 0) return BMC_OK;
-    BMC_CK(ctx, cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
-    return BMC_OK;
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (bytes == 0) return BMC_OK;
+        BMC_CK(ctx, cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_copy_to_device(bmc_ctx* ctx, void* dev, const void* host, size_t bytes) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if (bytes == 0) return BMC_OK;
-    BMC_CK(ctx, cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
-    return BMC_OK;
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (bytes == 0) return BMC_OK;
+        BMC_CK(ctx, cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        BMC_CK(ctx, cudaStreamSynchronize(ctx->stream));
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_draw_device(bmc_ctx* ctx, const bmc_model* model, uint64_t first, size_t n,
                          const bmc_world* world, double* terms, bmc_sample* samples,
                          uint64_t* clamp_count) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if (n == 0) return fail(ctx, BMC_E_CONFIG, "samples: must be >= 1");  // sampling.cpp:68-70
-    if (!model || !world) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_draw_device: null argument");
-    bmc_run_opts o{};
-    o.sampler = 2;
-    bool dev = false;
-    if ((rc = bmc::use_device_sampler(ctx, o, &dev)) != BMC_OK) return rc;
-    bmc::DrawArgs a = bmc::draw_args(*model, first, n, *world);
-    if (terms) {
-        a.v0 = terms;
-        a.brake_floor = terms + n;
-        a.drag = terms + 2 * n;
-        a.grade = terms + 3 * n;
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (n == 0) return fail(ctx, BMC_E_CONFIG, "samples: must be >= 1");  // sampling.cpp:68-70
+        if (!model || !world) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_draw_device: null argument");
+        bmc_run_opts o{};
+        o.sampler = 2;
+        bool dev = false;
+        if ((rc = bmc::use_device_sampler(ctx, o, &dev)) != BMC_OK) return rc;
+        bmc::DrawArgs a = bmc::draw_args(*model, first, n, *world);
+        if (terms) {
+            a.v0 = terms;
+            a.brake_floor = terms + n;
+            a.drag = terms + 2 * n;
+            a.grade = terms + 3 * n;
+        }
+        a.samples = reinterpret_cast<double*>(samples);
+        BMC_CK(ctx, ctx->draw_ctr.reserve(16));
+        BMC_CK(ctx, cudaMemsetAsync(ctx->draw_ctr.p, 0, 16, ctx->stream));
+        a.clamps = ctx->draw_ctr.as<unsigned long long>();
+        a.flags = reinterpret_cast<unsigned int*>(ctx->draw_ctr.as<char>() + 8);
+        BMC_CK(ctx, bmc::launch_draw_terms(a, ctx->sms, ctx->stream));
+        ctx->last_launches = 1;
+        return bmc::finish_draw(ctx, ctx->draw_ctr, clamp_count);
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    a.samples = reinterpret_cast<double*>(samples);
-    BMC_CK(ctx, ctx->draw_ctr.reserve(16));
-    BMC_CK(ctx, cudaMemsetAsync(ctx->draw_ctr.p, 0, 16, ctx->stream));
-    a.clamps = ctx->draw_ctr.as<unsigned long long>();
-    a.flags = reinterpret_cast<unsigned int*>(ctx->draw_ctr.as<char>() + 8);
-    BMC_CK(ctx, bmc::launch_draw_terms(a, ctx->sms, ctx->stream));
-    ctx->last_launches = 1;
-    return bmc::finish_draw(ctx, ctx->draw_ctr, clamp_count);
 }
 
 int bmc_cuda_last_launches(bmc_ctx* ctx, uint32_t* launches) {
-    if (!ctx || !launches) return BMC_E_CONFIG;
-    *launches = ctx->last_launches;
-    return BMC_OK;
+    try {
+        if (!ctx || !launches) return BMC_E_CONFIG;
+        *launches = ctx->last_launches;
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_run(bmc_ctx* ctx, const bmc_sample* samples, size_t n, const bmc_world* world,
                  const bmc_run_opts* opts, bmc_result* out, bmc_run_info* info) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if (n == 0) return fail(ctx, BMC_E_CONFIG, "batch: must be non-empty");  // backends.cpp:41-43
-    if (!samples || !world || !out) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_run: null argument");
-    bmc::WorldDerived d{};
-    std::string err;
-    if ((rc = bmc::derive_world(*world, &d, &err)) != BMC_OK) return fail(ctx, rc, err);
-    const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
-    return bmc::run_pipeline(ctx, *world, d, o, n, samples, nullptr, 0, out, nullptr, info, nullptr);
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (n == 0) return fail(ctx, BMC_E_CONFIG, "batch: must be non-empty");  // backends.cpp:41-43
+        if (!samples || !world || !out) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_run: null argument");
+        bmc::WorldDerived d{};
+        std::string err;
+        if ((rc = bmc::derive_world(*world, &d, &err)) != BMC_OK) return fail(ctx, rc, err);
+        const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
+        return bmc::run_pipeline(ctx, *world, d, o, n, samples, nullptr, 0, out, nullptr, info, nullptr);
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_run_model(bmc_ctx* ctx, const bmc_model* model, uint64_t first, size_t n,
                        const bmc_world* world, const bmc_run_opts* opts, bmc_result* host_out,
                        const bmc_outputs* dev_out, uint64_t* clamp_count, bmc_run_info* info) {
-    return bmc_cuda_run_model_stats(ctx, model, first, n, world, opts, host_out, dev_out,
-                                    clamp_count, info, nullptr);
+    try {
+        return bmc_cuda_run_model_stats(ctx, model, first, n, world, opts, host_out, dev_out,
+                                        clamp_count, info, nullptr);
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_run_model_stats(bmc_ctx* ctx, const bmc_model* model, uint64_t first, size_t n,
                              const bmc_world* world, const bmc_run_opts* opts, bmc_result* host_out,
                              const bmc_outputs* dev_out, uint64_t* clamp_count, bmc_run_info* info,
                              bmc_stats_stage* st) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if (n == 0) return fail(ctx, BMC_E_CONFIG, "samples: must be >= 1");  // sampling.cpp:68-70
-    if (!model || !world) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_run_model: null argument");
-    if ((host_out == nullptr) == (dev_out == nullptr)) {
-        return fail(ctx, BMC_E_CONFIG, "bmc_cuda_run_model: exactly one of host_out / dev_out");
-    }
-    bmc::WorldDerived d{};
-    std::string err;
-    if ((rc = bmc::derive_world(*world, &d, &err)) != BMC_OK) return fail(ctx, rc, err);
-    const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
-    bmc::P1Args p1{};
-    if (st) {
-        if (!bmc::stats_p1_args(st, &p1)) {
-            return fail(ctx, BMC_E_RANGE, "risk.headways: at most 4096 when fused into a streamed run");
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (n == 0) return fail(ctx, BMC_E_CONFIG, "samples: must be >= 1");  // sampling.cpp:68-70
+        if (!model || !world) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_run_model: null argument");
+        if ((host_out == nullptr) == (dev_out == nullptr)) {
+            return fail(ctx, BMC_E_CONFIG, "bmc_cuda_run_model: exactly one of host_out / dev_out");
         }
-        if (bmc::stats_max_n(st) < n) {
-            return fail(ctx, BMC_E_CONFIG, "stats: more results than the stage was sized for");
+        bmc::WorldDerived d{};
+        std::string err;
+        if ((rc = bmc::derive_world(*world, &d, &err)) != BMC_OK) return fail(ctx, rc, err);
+        const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
+        bmc::P1Args p1{};
+        if (st) {
+            if (!bmc::stats_p1_args(st, &p1)) {
+                return fail(ctx, BMC_E_RANGE, "risk.headways: at most 4096 when fused into a streamed run");
+            }
+            if (bmc::stats_max_n(st) < n) {
+                return fail(ctx, BMC_E_CONFIG, "stats: more results than the stage was sized for");
+            }
         }
+        // chunks run on the slot streams; the stage was begun on ctx->stream,
+        // which run_pipeline synchronises before the first chunk
+        return bmc::run_pipeline(ctx, *world, d, o, n, nullptr, model, first, host_out, dev_out, info,
+                                 clamp_count, st ? &p1 : nullptr);
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    // chunks run on the slot streams; the stage was begun on ctx->stream,
-    // which run_pipeline synchronises before the first chunk
-    return bmc::run_pipeline(ctx, *world, d, o, n, nullptr, model, first, host_out, dev_out, info,
-                             clamp_count, st ? &p1 : nullptr);
 }
 
 }  // extern "C"

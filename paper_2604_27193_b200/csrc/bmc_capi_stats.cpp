@@ -411,12 +411,16 @@ size_t stats_max_n(const bmc_stats_stage* st) { return st->max_n; }
 extern "C" {
 
 int bmc_stats_create(bmc_ctx* ctx, const bmc_stats_req* req, size_t max_n, bmc_stats_stage** out) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if (!out) return fail(ctx, BMC_E_CONFIG, "bmc_stats_create: null output");
-    *out = nullptr;
-    return bmc::stage_create(ctx, req, max_n, out);
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (!out) return fail(ctx, BMC_E_CONFIG, "bmc_stats_create: null output");
+        *out = nullptr;
+        return bmc::stage_create(ctx, req, max_n, out);
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 void bmc_stats_destroy(bmc_stats_stage* st) {
@@ -430,95 +434,115 @@ void bmc_stats_destroy(bmc_stats_stage* st) {
 }
 
 int bmc_stats_begin(bmc_stats_stage* st, void* stream) {
-    if (!st) return fail(nullptr, BMC_E_CONFIG, "bmc_stats_begin: null stage");
-    int rc = bmc::prepare(st->ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(st->ctx->mu);
-    return bmc::stage_begin(st, bmc::stream_of(st, stream));
+    try {
+        if (!st) return fail(nullptr, BMC_E_CONFIG, "bmc_stats_begin: null stage");
+        int rc = bmc::prepare(st->ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(st->ctx->mu);
+        return bmc::stage_begin(st, bmc::stream_of(st, stream));
+    } catch (...) {
+        return bmc::abi_exception();
+    }
 }
 
 int bmc_stats_accumulate(bmc_stats_stage* st, const double* d, const uint8_t* hz, size_t n,
                          void* stream) {
-    if (!st) return fail(nullptr, BMC_E_CONFIG, "bmc_stats_accumulate: null stage");
-    int rc = bmc::prepare(st->ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(st->ctx->mu);
-    if (n && !d) return fail(st->ctx, BMC_E_CONFIG, "bmc_stats_accumulate: null outputs");
-    if (n > st->max_n) return fail(st->ctx, BMC_E_CONFIG, "stats: more results than the stage was sized for");
-    return bmc::stage_accumulate(st, d, hz, n, bmc::stream_of(st, stream));
+    try {
+        if (!st) return fail(nullptr, BMC_E_CONFIG, "bmc_stats_accumulate: null stage");
+        int rc = bmc::prepare(st->ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(st->ctx->mu);
+        if (n && !d) return fail(st->ctx, BMC_E_CONFIG, "bmc_stats_accumulate: null outputs");
+        if (n > st->max_n) return fail(st->ctx, BMC_E_CONFIG, "stats: more results than the stage was sized for");
+        return bmc::stage_accumulate(st, d, hz, n, bmc::stream_of(st, stream));
+    } catch (...) {
+        return bmc::abi_exception();
+    }
 }
 
 int bmc_stats_finish(bmc_stats_stage* st, const double* d, const uint8_t* hz, size_t n,
                      const bmc_merge* merge, bmc_stats* out, void* stream) {
-    if (!st || !out) return fail(st ? st->ctx : nullptr, BMC_E_CONFIG, "bmc_stats_finish: null argument");
-    int rc = bmc::prepare(st->ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(st->ctx->mu);
-    if (n && !d) return fail(st->ctx, BMC_E_CONFIG, "bmc_stats_finish: null outputs");
-    if (n > st->max_n) return fail(st->ctx, BMC_E_CONFIG, "stats: more results than the stage was sized for");
-    return bmc::stage_finish(st, d, hz, n, merge, out, bmc::stream_of(st, stream));
+    try {
+        if (!st || !out) return fail(st ? st->ctx : nullptr, BMC_E_CONFIG, "bmc_stats_finish: null argument");
+        int rc = bmc::prepare(st->ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(st->ctx->mu);
+        if (n && !d) return fail(st->ctx, BMC_E_CONFIG, "bmc_stats_finish: null outputs");
+        if (n > st->max_n) return fail(st->ctx, BMC_E_CONFIG, "stats: more results than the stage was sized for");
+        return bmc::stage_finish(st, d, hz, n, merge, out, bmc::stream_of(st, stream));
+    } catch (...) {
+        return bmc::abi_exception();
+    }
 }
 
 int bmc_cuda_stats(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n,
                    const bmc_stats_req* req, bmc_stats* out) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    if (!out) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_stats: null output");
-    if (n == 0) {
-        return fail(ctx, BMC_E_CONFIG, req && req->summarize ? "summarize: needs at least one result"
-                                                             : "risk: needs at least one result");
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        if (!out) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_stats: null output");
+        if (n == 0) {
+            return fail(ctx, BMC_E_CONFIG, req && req->summarize ? "summarize: needs at least one result"
+                                                                 : "risk: needs at least one result");
+        }
+        if (!d) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_stats: null outputs");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        // reuse the context's cached stage when the resolved request (and so the
+        // layout and candidate capacity) is the same; the stage's memory is
+        // allocated once per request shape, not per call
+        bmc::StatsConfig cfg;
+        std::string err;
+        if ((rc = bmc::resolve_request(req, n, &cfg, &err)) != BMC_OK) return fail(ctx, rc, err);
+        bmc_stats_stage* st = ctx->stats_cache;
+        if (!st || !bmc::same_config(st->cfg, cfg) || st->max_n < n) {
+            if (st) bmc_stats_destroy(st);
+            ctx->stats_cache = nullptr;
+            if ((rc = bmc::stage_create(ctx, req, n, &st)) != BMC_OK) return rc;
+            ctx->stats_cache = st;
+        }
+        cudaStream_t s = ctx->stream;
+        if (ctx->scratch_used) BMC_CK(ctx, cudaStreamWaitEvent(s, ctx->scratch_done, 0));
+        if ((rc = bmc::stage_begin(st, s)) != BMC_OK) return rc;
+        if ((rc = bmc::stage_accumulate(st, d, hz, n, s)) != BMC_OK) return rc;
+        return bmc::stage_finish(st, d, hz, n, nullptr, out, s);
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    if (!d) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_stats: null outputs");
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    // reuse the context's cached stage when the resolved request (and so the
-    // layout and candidate capacity) is the same; the stage's memory is
-    // allocated once per request shape, not per call
-    bmc::StatsConfig cfg;
-    std::string err;
-    if ((rc = bmc::resolve_request(req, n, &cfg, &err)) != BMC_OK) return fail(ctx, rc, err);
-    bmc_stats_stage* st = ctx->stats_cache;
-    if (!st || !bmc::same_config(st->cfg, cfg) || st->max_n < n) {
-        if (st) bmc_stats_destroy(st);
-        ctx->stats_cache = nullptr;
-        if ((rc = bmc::stage_create(ctx, req, n, &st)) != BMC_OK) return rc;
-        ctx->stats_cache = st;
-    }
-    cudaStream_t s = ctx->stream;
-    if (ctx->scratch_used) BMC_CK(ctx, cudaStreamWaitEvent(s, ctx->scratch_done, 0));
-    if ((rc = bmc::stage_begin(st, s)) != BMC_OK) return rc;
-    if ((rc = bmc::stage_accumulate(st, d, hz, n, s)) != BMC_OK) return rc;
-    return bmc::stage_finish(st, d, hz, n, nullptr, out, s);
 }
 
 int bmc_cuda_rollout_stats(bmc_ctx* ctx, const bmc_terms* terms, size_t n, const bmc_world* world,
                            const bmc_run_opts* opts, const bmc_outputs* out,
                            unsigned long long* total_steps_dev, bmc_stats_stage* st, void* stream) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if (!terms || !world || !out) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_rollout_device: null argument");
-    if (n == 0) return fail(ctx, BMC_E_CONFIG, "batch: must be non-empty");
-    if (st && st->ctx != ctx) return fail(ctx, BMC_E_CONFIG, "stats: stage belongs to another context");
-    if (st && n > st->max_n) return fail(ctx, BMC_E_CONFIG, "stats: more results than the stage was sized for");
-    bmc::WorldDerived d{};
-    std::string err;
-    if ((rc = bmc::derive_world(*world, &d, &err)) != BMC_OK) return fail(ctx, rc, err);
-    const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-    bmc::Plan plan;
-    if ((rc = bmc::make_plan(ctx, d, o, n, &plan)) != BMC_OK) return rc;
-    bmc::P1Args p1{};
-    if (st) {
-        st->exceed_pending = !bmc::stats_p1_args(st, &p1);
-        bmc::fit_stats_plan(&plan, p1);
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (!terms || !world || !out) return fail(ctx, BMC_E_CONFIG, "bmc_cuda_rollout_device: null argument");
+        if (n == 0) return fail(ctx, BMC_E_CONFIG, "batch: must be non-empty");
+        if (st && st->ctx != ctx) return fail(ctx, BMC_E_CONFIG, "stats: stage belongs to another context");
+        if (st && n > st->max_n) return fail(ctx, BMC_E_CONFIG, "stats: more results than the stage was sized for");
+        bmc::WorldDerived d{};
+        std::string err;
+        if ((rc = bmc::derive_world(*world, &d, &err)) != BMC_OK) return fail(ctx, rc, err);
+        const bmc_run_opts o = opts ? *opts : bmc_run_opts{};
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        bmc::Plan plan;
+        if ((rc = bmc::make_plan(ctx, d, o, n, &plan)) != BMC_OK) return rc;
+        bmc::P1Args p1{};
+        if (st) {
+            st->exceed_pending = !bmc::stats_p1_args(st, &p1);
+            bmc::fit_stats_plan(&plan, p1);
+        }
+        ctx->last_launches = 0;
+        if (ctx->scratch_used) BMC_CK(ctx, cudaStreamWaitEvent(s, ctx->scratch_done, 0));
+        rc = bmc::enqueue_rollout(ctx, plan, ctx->scratch, *terms, n, *out, total_steps_dev, s, &ctx->kev,
+                                  &ctx->last_launches, st ? &p1 : nullptr);
+        BMC_CK(ctx, cudaEventRecord(ctx->scratch_done, s));
+        ctx->scratch_used = true;
+        return rc;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    ctx->last_launches = 0;
-    if (ctx->scratch_used) BMC_CK(ctx, cudaStreamWaitEvent(s, ctx->scratch_done, 0));
-    rc = bmc::enqueue_rollout(ctx, plan, ctx->scratch, *terms, n, *out, total_steps_dev, s, &ctx->kev,
-                              &ctx->last_launches, st ? &p1 : nullptr);
-    BMC_CK(ctx, cudaEventRecord(ctx->scratch_done, s));
-    ctx->scratch_used = true;
-    return rc;
 }
 
 }  // extern "C"
@@ -528,143 +552,159 @@ extern "C" {
 int bmc_cuda_order_stats(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n,
                          int exclude_horizon, const uint64_t* ranks, size_t m, double* out,
                          uint64_t* count_out) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
-    if (!d || (m && (!ranks || !out))) return fail(ctx, BMC_E_CONFIG, "order_stats: null argument");
-    if (exclude_horizon && !hz) return fail(ctx, BMC_E_CONFIG, "order_stats: horizon flags required");
-    ctx->last_launches = 0;
-    if (n == 0) return fail(ctx, BMC_E_CONFIG, "risk: needs at least one result");
-    return bmc::select_ranks(ctx, d, hz, n, exclude_horizon, ranks, m, out, count_out);
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
+        if (!d || (m && (!ranks || !out))) return fail(ctx, BMC_E_CONFIG, "order_stats: null argument");
+        if (exclude_horizon && !hz) return fail(ctx, BMC_E_CONFIG, "order_stats: horizon flags required");
+        ctx->last_launches = 0;
+        if (n == 0) return fail(ctx, BMC_E_CONFIG, "risk: needs at least one result");
+        return bmc::select_ranks(ctx, d, hz, n, exclude_horizon, ranks, m, out, count_out);
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_summarize(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n, double bin_width,
                        bmc_summary* out, uint64_t* hist, size_t hist_cap) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    // analysis.cpp:14-19
-    if (n == 0) return fail(ctx, BMC_E_CONFIG, "summarize: needs at least one result");
-    if (!(bin_width > 0.0)) return fail(ctx, BMC_E_CONFIG, "outputs.bin_width: must be > 0");
-    if (!d || !out) return fail(ctx, BMC_E_CONFIG, "summarize: null argument");
-    bmc_stats_req req{};
-    req.summarize = 1;
-    req.bin_width = bin_width;
-    bmc_stats st{};
-    st.histogram = hist;
-    st.histogram_cap = hist ? hist_cap : 0;
-    rc = bmc_cuda_stats(ctx, d, hz, n, &req, &st);
-    if (rc == BMC_OK || rc == BMC_E_RANGE) *out = st.summary;
-    return rc;
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        // analysis.cpp:14-19
+        if (n == 0) return fail(ctx, BMC_E_CONFIG, "summarize: needs at least one result");
+        if (!(bin_width > 0.0)) return fail(ctx, BMC_E_CONFIG, "outputs.bin_width: must be > 0");
+        if (!d || !out) return fail(ctx, BMC_E_CONFIG, "summarize: null argument");
+        bmc_stats_req req{};
+        req.summarize = 1;
+        req.bin_width = bin_width;
+        bmc_stats st{};
+        st.histogram = hist;
+        st.histogram_cap = hist ? hist_cap : 0;
+        rc = bmc_cuda_stats(ctx, d, hz, n, &req, &st);
+        if (rc == BMC_OK || rc == BMC_E_RANGE) *out = st.summary;
+        return rc;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_exceedance_ttc_noise(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n,
                                   uint64_t first, uint64_t noise_seed, double sigma,
                                   const double* ttc, size_t m, double closing_speed,
                                   uint64_t* counts) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
-    if (n == 0) return fail(ctx, BMC_E_CONFIG, "risk: needs at least one result");
-    if (m == 0) return BMC_OK;
-    if (!d || !ttc || !counts) return fail(ctx, BMC_E_CONFIG, "exceedance: null argument");
-    if (!(closing_speed > 0.0)) return fail(ctx, BMC_E_CONFIG, "risk.closing_speed: must be > 0");
-    if (!(sigma >= 0.0) || !std::isfinite(sigma)) {
-        return fail(ctx, BMC_E_CONFIG, "risk.sensor_noise: must be finite and >= 0");
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
+        if (n == 0) return fail(ctx, BMC_E_CONFIG, "risk: needs at least one result");
+        if (m == 0) return BMC_OK;
+        if (!d || !ttc || !counts) return fail(ctx, BMC_E_CONFIG, "exceedance: null argument");
+        if (!(closing_speed > 0.0)) return fail(ctx, BMC_E_CONFIG, "risk.closing_speed: must be > 0");
+        if (!(sigma >= 0.0) || !std::isfinite(sigma)) {
+            return fail(ctx, BMC_E_CONFIG, "risk.sensor_noise: must be finite and >= 0");
+        }
+        if (m > static_cast<size_t>(bmc::kNoiseMaxThresholds)) {
+            return fail(ctx, BMC_E_RANGE, "risk.ttc: at most 1024 thresholds");
+        }
+        for (size_t j = 0; j < m; ++j) {
+            if (!std::isfinite(ttc[j])) return fail(ctx, BMC_E_CONFIG, "risk.ttc: must be finite");
+        }
+        std::string why;
+        if (!bmc::device_sampler_supported(&why)) {
+            return fail(ctx, BMC_E_CONFIG, "risk.sensor_noise: " + why);
+        }
+        ctx->last_launches = 0;
+        std::vector<size_t> order(m);
+        std::iota(order.begin(), order.end(), size_t{0});
+        std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return ttc[a] < ttc[b]; });
+        std::vector<double> sorted(m);
+        for (size_t j = 0; j < m; ++j) sorted[j] = ttc[order[j]];
+        cudaStream_t s = ctx->stream;
+        BMC_CK(ctx, ctx->sorted_h.reserve(m * sizeof(double)));
+        BMC_CK(ctx, ctx->buckets.reserve((m + 1) * sizeof(unsigned long long)));
+        BMC_CK(ctx, ctx->draw_ctr.reserve(16));
+        BMC_CK(ctx, cudaMemcpyAsync(ctx->sorted_h.p, sorted.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
+        BMC_CK(ctx, cudaMemsetAsync(ctx->buckets.p, 0, (m + 1) * sizeof(unsigned long long), s));
+        BMC_CK(ctx, cudaMemsetAsync(ctx->draw_ctr.p, 0, 16, s));
+        bmc::NoiseExceedArgs a{};
+        a.d = d;
+        a.hz = hz;
+        a.n = n;
+        a.first = first;
+        a.seed = noise_seed;
+        a.sigma = sigma;
+        a.closing = closing_speed;
+        a.ttc = ctx->sorted_h.as<double>();
+        a.m = static_cast<int>(m);
+        a.buckets = ctx->buckets.as<unsigned long long>();
+        a.flags = reinterpret_cast<unsigned int*>(ctx->draw_ctr.as<char>() + 8);
+        BMC_CK(ctx, bmc::launch_noise_exceed(a, ctx->sms, s));
+        std::vector<unsigned long long> b(m + 1);
+        BMC_CK(ctx, cudaMemcpyAsync(b.data(), ctx->buckets.p, (m + 1) * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, s));
+        if ((rc = bmc::finish_draw(ctx, ctx->draw_ctr, nullptr)) != BMC_OK) return rc;  // syncs s
+        ctx->last_launches = 1;
+        uint64_t suffix = 0;
+        std::vector<uint64_t> ex(m);
+        for (size_t j = m; j-- > 0;) {
+            suffix += b[j + 1];
+            ex[j] = suffix;
+        }
+        for (size_t j = 0; j < m; ++j) counts[order[j]] = ex[j];
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    if (m > static_cast<size_t>(bmc::kNoiseMaxThresholds)) {
-        return fail(ctx, BMC_E_RANGE, "risk.ttc: at most 1024 thresholds");
-    }
-    for (size_t j = 0; j < m; ++j) {
-        if (!std::isfinite(ttc[j])) return fail(ctx, BMC_E_CONFIG, "risk.ttc: must be finite");
-    }
-    std::string why;
-    if (!bmc::device_sampler_supported(&why)) {
-        return fail(ctx, BMC_E_CONFIG, "risk.sensor_noise: " + why);
-    }
-    ctx->last_launches = 0;
-    std::vector<size_t> order(m);
-    std::iota(order.begin(), order.end(), size_t{0});
-    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return ttc[a] < ttc[b]; });
-    std::vector<double> sorted(m);
-    for (size_t j = 0; j < m; ++j) sorted[j] = ttc[order[j]];
-    cudaStream_t s = ctx->stream;
-    BMC_CK(ctx, ctx->sorted_h.reserve(m * sizeof(double)));
-    BMC_CK(ctx, ctx->buckets.reserve((m + 1) * sizeof(unsigned long long)));
-    BMC_CK(ctx, ctx->draw_ctr.reserve(16));
-    BMC_CK(ctx, cudaMemcpyAsync(ctx->sorted_h.p, sorted.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
-    BMC_CK(ctx, cudaMemsetAsync(ctx->buckets.p, 0, (m + 1) * sizeof(unsigned long long), s));
-    BMC_CK(ctx, cudaMemsetAsync(ctx->draw_ctr.p, 0, 16, s));
-    bmc::NoiseExceedArgs a{};
-    a.d = d;
-    a.hz = hz;
-    a.n = n;
-    a.first = first;
-    a.seed = noise_seed;
-    a.sigma = sigma;
-    a.closing = closing_speed;
-    a.ttc = ctx->sorted_h.as<double>();
-    a.m = static_cast<int>(m);
-    a.buckets = ctx->buckets.as<unsigned long long>();
-    a.flags = reinterpret_cast<unsigned int*>(ctx->draw_ctr.as<char>() + 8);
-    BMC_CK(ctx, bmc::launch_noise_exceed(a, ctx->sms, s));
-    std::vector<unsigned long long> b(m + 1);
-    BMC_CK(ctx, cudaMemcpyAsync(b.data(), ctx->buckets.p, (m + 1) * sizeof(unsigned long long),
-                                cudaMemcpyDeviceToHost, s));
-    if ((rc = bmc::finish_draw(ctx, ctx->draw_ctr, nullptr)) != BMC_OK) return rc;  // syncs s
-    ctx->last_launches = 1;
-    uint64_t suffix = 0;
-    std::vector<uint64_t> ex(m);
-    for (size_t j = m; j-- > 0;) {
-        suffix += b[j + 1];
-        ex[j] = suffix;
-    }
-    for (size_t j = 0; j < m; ++j) counts[order[j]] = ex[j];
-    return BMC_OK;
 }
 
 int bmc_cuda_exceedance(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n,
                         const double* headways, size_t m, uint64_t* counts) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
-    if (n == 0) return fail(ctx, BMC_E_CONFIG, "risk: needs at least one result");
-    if (m == 0) return BMC_OK;
-    if (!d || !headways || !counts) return fail(ctx, BMC_E_CONFIG, "exceedance: null argument");
-    for (size_t j = 0; j < m; ++j) {
-        if (!(headways[j] >= 0.0)) return fail(ctx, BMC_E_CONFIG, "risk.headway: must be >= 0");
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
+        if (n == 0) return fail(ctx, BMC_E_CONFIG, "risk: needs at least one result");
+        if (m == 0) return BMC_OK;
+        if (!d || !headways || !counts) return fail(ctx, BMC_E_CONFIG, "exceedance: null argument");
+        for (size_t j = 0; j < m; ++j) {
+            if (!(headways[j] >= 0.0)) return fail(ctx, BMC_E_CONFIG, "risk.headway: must be >= 0");
+        }
+        if (m > (size_t{1} << 30)) return fail(ctx, BMC_E_RANGE, "exceedance: too many headways");
+        ctx->last_launches = 0;
+        std::vector<size_t> order(m);
+        std::iota(order.begin(), order.end(), size_t{0});
+        std::stable_sort(order.begin(), order.end(),
+                         [&](size_t a, size_t b) { return headways[a] < headways[b]; });
+        std::vector<double> sorted(m);
+        for (size_t j = 0; j < m; ++j) sorted[j] = headways[order[j]];
+        cudaStream_t s = ctx->stream;
+        BMC_CK(ctx, ctx->sorted_h.reserve(m * sizeof(double)));
+        BMC_CK(ctx, ctx->buckets.reserve((m + 1) * sizeof(unsigned long long)));
+        BMC_CK(ctx, cudaMemcpyAsync(ctx->sorted_h.p, sorted.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
+        BMC_CK(ctx, cudaMemsetAsync(ctx->buckets.p, 0, (m + 1) * sizeof(unsigned long long), s));
+        BMC_CK(ctx, bmc::launch_exceed(d, hz, n, ctx->sorted_h.as<double>(), static_cast<int>(m),
+                                       ctx->buckets.as<unsigned long long>(), s));
+        std::vector<unsigned long long> b(m + 1);
+        BMC_CK(ctx, cudaMemcpyAsync(b.data(), ctx->buckets.p, (m + 1) * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, s));
+        BMC_CK(ctx, cudaStreamSynchronize(s));
+        ctx->last_launches = 1;
+        // exceed(sorted j) = #{p > j} = suffix sum of buckets (j+1 .. m)
+        uint64_t suffix = 0;
+        std::vector<uint64_t> ex(m);
+        for (size_t j = m; j-- > 0;) {
+            suffix += b[j + 1];
+            ex[j] = suffix;
+        }
+        for (size_t j = 0; j < m; ++j) counts[order[j]] = ex[j];
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    if (m > (size_t{1} << 30)) return fail(ctx, BMC_E_RANGE, "exceedance: too many headways");
-    ctx->last_launches = 0;
-    std::vector<size_t> order(m);
-    std::iota(order.begin(), order.end(), size_t{0});
-    std::stable_sort(order.begin(), order.end(),
-                     [&](size_t a, size_t b) { return headways[a] < headways[b]; });
-    std::vector<double> sorted(m);
-    for (size_t j = 0; j < m; ++j) sorted[j] = headways[order[j]];
-    cudaStream_t s = ctx->stream;
-    BMC_CK(ctx, ctx->sorted_h.reserve(m * sizeof(double)));
-    BMC_CK(ctx, ctx->buckets.reserve((m + 1) * sizeof(unsigned long long)));
-    BMC_CK(ctx, cudaMemcpyAsync(ctx->sorted_h.p, sorted.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
-    BMC_CK(ctx, cudaMemsetAsync(ctx->buckets.p, 0, (m + 1) * sizeof(unsigned long long), s));
-    BMC_CK(ctx, bmc::launch_exceed(d, hz, n, ctx->sorted_h.as<double>(), static_cast<int>(m),
-                                   ctx->buckets.as<unsigned long long>(), s));
-    std::vector<unsigned long long> b(m + 1);
-    BMC_CK(ctx, cudaMemcpyAsync(b.data(), ctx->buckets.p, (m + 1) * sizeof(unsigned long long),
-                                cudaMemcpyDeviceToHost, s));
-    BMC_CK(ctx, cudaStreamSynchronize(s));
-    ctx->last_launches = 1;
-    // exceed(sorted j) = #{p > j} = suffix sum of buckets (j+1 .. m)
-    uint64_t suffix = 0;
-    std::vector<uint64_t> ex(m);
-    for (size_t j = m; j-- > 0;) {
-        suffix += b[j + 1];
-        ex[j] = suffix;
-    }
-    for (size_t j = 0; j < m; ++j) counts[order[j]] = ex[j];
-    return BMC_OK;
 }
 
 // ----------------------------------------------------------------------
@@ -674,120 +714,136 @@ int bmc_cuda_exceedance(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t
 
 int bmc_cuda_partials(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n,
                       bmc_partials* out) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
-    if (!d || !out) return fail(ctx, BMC_E_CONFIG, "partials: null argument");
-    bmc_partials p;
-    std::memset(&p, 0, sizeof p);
-    p.min = std::numeric_limits<double>::infinity();
-    p.max = -std::numeric_limits<double>::infinity();
-    ctx->last_launches = 0;
-    if (n > 0) {
-        cudaStream_t s = ctx->stream;
-        const int P = bmc::stats_partials(n);
-        BMC_CK(ctx, ctx->partials.reserve(static_cast<size_t>(P) * sizeof(bmc::BlockPartial)));
-        std::vector<bmc::BlockPartial> parts(P);
-        BMC_CK(ctx, bmc::launch_reduce(d, hz, n, ctx->partials.as<bmc::BlockPartial>(), s));
-        BMC_CK(ctx, cudaMemcpyAsync(parts.data(), ctx->partials.p, P * sizeof(bmc::BlockPartial),
-                                    cudaMemcpyDeviceToHost, s));
-        BMC_CK(ctx, cudaStreamSynchronize(s));
-        ctx->last_launches = 1;
-        bmc::DDh sum;
-        for (const auto& q : parts) {
-            p.min = std::fmin(p.min, q.min);
-            p.max = std::fmax(p.max, q.max);
-            sum = bmc::dd_merge_h(sum, q.sum_hi, q.sum_lo);
-            p.horizon_count += q.horizon;
-            p.count += q.count;
-            p.any_nan |= q.nan;
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
+        if (!d || !out) return fail(ctx, BMC_E_CONFIG, "partials: null argument");
+        bmc_partials p;
+        std::memset(&p, 0, sizeof p);
+        p.min = std::numeric_limits<double>::infinity();
+        p.max = -std::numeric_limits<double>::infinity();
+        ctx->last_launches = 0;
+        if (n > 0) {
+            cudaStream_t s = ctx->stream;
+            const int P = bmc::stats_partials(n);
+            BMC_CK(ctx, ctx->partials.reserve(static_cast<size_t>(P) * sizeof(bmc::BlockPartial)));
+            std::vector<bmc::BlockPartial> parts(P);
+            BMC_CK(ctx, bmc::launch_reduce(d, hz, n, ctx->partials.as<bmc::BlockPartial>(), s));
+            BMC_CK(ctx, cudaMemcpyAsync(parts.data(), ctx->partials.p, P * sizeof(bmc::BlockPartial),
+                                        cudaMemcpyDeviceToHost, s));
+            BMC_CK(ctx, cudaStreamSynchronize(s));
+            ctx->last_launches = 1;
+            bmc::DDh sum;
+            for (const auto& q : parts) {
+                p.min = std::fmin(p.min, q.min);
+                p.max = std::fmax(p.max, q.max);
+                sum = bmc::dd_merge_h(sum, q.sum_hi, q.sum_lo);
+                p.horizon_count += q.horizon;
+                p.count += q.count;
+                p.any_nan |= q.nan;
+            }
+            p.sum_hi = sum.hi;
+            p.sum_lo = sum.lo;
         }
-        p.sum_hi = sum.hi;
-        p.sum_lo = sum.lo;
+        *out = p;
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    *out = p;
-    return BMC_OK;
 }
 
 int bmc_cuda_moments(bmc_ctx* ctx, const double* d, size_t n, double mean, double* m2m3) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
-    if (!d || !m2m3) return fail(ctx, BMC_E_CONFIG, "moments: null argument");
-    ctx->last_launches = 0;
-    bmc::DDh m2, m3;
-    if (n > 0) {
-        cudaStream_t s = ctx->stream;
-        const int P = bmc::stats_partials(n);
-        BMC_CK(ctx, ctx->partials.reserve(static_cast<size_t>(P) * sizeof(bmc::MomentPartial)));
-        std::vector<bmc::MomentPartial> mom(P);
-        BMC_CK(ctx, bmc::launch_moments(d, n, mean, ctx->partials.as<bmc::MomentPartial>(), s));
-        BMC_CK(ctx, cudaMemcpyAsync(mom.data(), ctx->partials.p, P * sizeof(bmc::MomentPartial),
-                                    cudaMemcpyDeviceToHost, s));
-        BMC_CK(ctx, cudaStreamSynchronize(s));
-        ctx->last_launches = 1;
-        for (const auto& q : mom) {
-            m2 = bmc::dd_merge_h(m2, q.m2_hi, q.m2_lo);
-            m3 = bmc::dd_merge_h(m3, q.m3_hi, q.m3_lo);
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
+        if (!d || !m2m3) return fail(ctx, BMC_E_CONFIG, "moments: null argument");
+        ctx->last_launches = 0;
+        bmc::DDh m2, m3;
+        if (n > 0) {
+            cudaStream_t s = ctx->stream;
+            const int P = bmc::stats_partials(n);
+            BMC_CK(ctx, ctx->partials.reserve(static_cast<size_t>(P) * sizeof(bmc::MomentPartial)));
+            std::vector<bmc::MomentPartial> mom(P);
+            BMC_CK(ctx, bmc::launch_moments(d, n, mean, ctx->partials.as<bmc::MomentPartial>(), s));
+            BMC_CK(ctx, cudaMemcpyAsync(mom.data(), ctx->partials.p, P * sizeof(bmc::MomentPartial),
+                                        cudaMemcpyDeviceToHost, s));
+            BMC_CK(ctx, cudaStreamSynchronize(s));
+            ctx->last_launches = 1;
+            for (const auto& q : mom) {
+                m2 = bmc::dd_merge_h(m2, q.m2_hi, q.m2_lo);
+                m3 = bmc::dd_merge_h(m3, q.m3_hi, q.m3_lo);
+            }
         }
+        m2m3[0] = m2.hi;
+        m2m3[1] = m2.lo;
+        m2m3[2] = m3.hi;
+        m2m3[3] = m3.lo;
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    m2m3[0] = m2.hi;
-    m2m3[1] = m2.lo;
-    m2m3[2] = m3.hi;
-    m2m3[3] = m3.lo;
-    return BMC_OK;
 }
 
 int bmc_cuda_histogram(bmc_ctx* ctx, const double* d, size_t n, double origin, double bin_width,
                        uint64_t bins, uint64_t* counts) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
-    if (!d || !counts) return fail(ctx, BMC_E_CONFIG, "histogram: null argument");
-    if (!(bin_width > 0.0)) return fail(ctx, BMC_E_CONFIG, "outputs.bin_width: must be > 0");
-    if (bins == 0 || bins > (uint64_t{1} << 28)) return fail(ctx, BMC_E_RANGE, "histogram: bins out of range");
-    ctx->last_launches = 0;
-    cudaStream_t s = ctx->stream;
-    BMC_CK(ctx, ctx->hist_buf.reserve(bins * sizeof(unsigned long long)));
-    BMC_CK(ctx, cudaMemsetAsync(ctx->hist_buf.p, 0, bins * sizeof(unsigned long long), s));
-    if (n > 0) {
-        BMC_CK(ctx, bmc::launch_hist(d, n, origin, bin_width, bins, ctx->hist_buf.as<unsigned long long>(), s));
-        ctx->last_launches = 1;
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
+        if (!d || !counts) return fail(ctx, BMC_E_CONFIG, "histogram: null argument");
+        if (!(bin_width > 0.0)) return fail(ctx, BMC_E_CONFIG, "outputs.bin_width: must be > 0");
+        if (bins == 0 || bins > (uint64_t{1} << 28)) return fail(ctx, BMC_E_RANGE, "histogram: bins out of range");
+        ctx->last_launches = 0;
+        cudaStream_t s = ctx->stream;
+        BMC_CK(ctx, ctx->hist_buf.reserve(bins * sizeof(unsigned long long)));
+        BMC_CK(ctx, cudaMemsetAsync(ctx->hist_buf.p, 0, bins * sizeof(unsigned long long), s));
+        if (n > 0) {
+            BMC_CK(ctx, bmc::launch_hist(d, n, origin, bin_width, bins, ctx->hist_buf.as<unsigned long long>(), s));
+            ctx->last_launches = 1;
+        }
+        BMC_CK(ctx, cudaMemcpyAsync(counts, ctx->hist_buf.p, bins * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        BMC_CK(ctx, cudaStreamSynchronize(s));
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    BMC_CK(ctx, cudaMemcpyAsync(counts, ctx->hist_buf.p, bins * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    BMC_CK(ctx, cudaStreamSynchronize(s));
-    return BMC_OK;
 }
 
 int bmc_cuda_select_pass(bmc_ctx* ctx, const double* d, const uint8_t* hz, size_t n,
                          int exclude_horizon, int shift, const uint64_t* prefixes, size_t m,
                          uint64_t* hist) {
-    int rc = bmc::prepare(ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
-    if (!d || !prefixes || !hist) return fail(ctx, BMC_E_CONFIG, "select_pass: null argument");
-    if (m < 1 || m > static_cast<size_t>(bmc::kMaxSelectTargets)) {
-        return fail(ctx, BMC_E_RANGE, "select_pass: 1..16 targets per pass");
+    try {
+        int rc = bmc::prepare(ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if ((rc = bmc::order_after_rollouts(ctx)) != BMC_OK) return rc;
+        if (!d || !prefixes || !hist) return fail(ctx, BMC_E_CONFIG, "select_pass: null argument");
+        if (m < 1 || m > static_cast<size_t>(bmc::kMaxSelectTargets)) {
+            return fail(ctx, BMC_E_RANGE, "select_pass: 1..16 targets per pass");
+        }
+        if (shift < 0 || shift > 56 || shift % 8 != 0) return fail(ctx, BMC_E_CONFIG, "select_pass: shift must be 0, 8, ..., 56");
+        ctx->last_launches = 0;
+        cudaStream_t s = ctx->stream;
+        BMC_CK(ctx, ctx->sel_pref.reserve(bmc::kMaxSelectTargets * sizeof(uint64_t)));
+        BMC_CK(ctx, ctx->sel_hist.reserve(bmc::kMaxSelectTargets * 256 * sizeof(unsigned long long)));
+        BMC_CK(ctx, cudaMemcpyAsync(ctx->sel_pref.p, prefixes, m * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        BMC_CK(ctx, cudaMemsetAsync(ctx->sel_hist.p, 0, m * 256 * sizeof(unsigned long long), s));
+        if (n > 0) {
+            BMC_CK(ctx, bmc::launch_select(d, hz, n, exclude_horizon, shift, ctx->sel_pref.as<uint64_t>(),
+                                           static_cast<int>(m), ctx->sel_hist.as<unsigned long long>(), s));
+            ctx->last_launches = 1;
+        }
+        BMC_CK(ctx, cudaMemcpyAsync(hist, ctx->sel_hist.p, m * 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        BMC_CK(ctx, cudaStreamSynchronize(s));
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception(ctx);
     }
-    if (shift < 0 || shift > 56 || shift % 8 != 0) return fail(ctx, BMC_E_CONFIG, "select_pass: shift must be 0, 8, ..., 56");
-    ctx->last_launches = 0;
-    cudaStream_t s = ctx->stream;
-    BMC_CK(ctx, ctx->sel_pref.reserve(bmc::kMaxSelectTargets * sizeof(uint64_t)));
-    BMC_CK(ctx, ctx->sel_hist.reserve(bmc::kMaxSelectTargets * 256 * sizeof(unsigned long long)));
-    BMC_CK(ctx, cudaMemcpyAsync(ctx->sel_pref.p, prefixes, m * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-    BMC_CK(ctx, cudaMemsetAsync(ctx->sel_hist.p, 0, m * 256 * sizeof(unsigned long long), s));
-    if (n > 0) {
-        BMC_CK(ctx, bmc::launch_select(d, hz, n, exclude_horizon, shift, ctx->sel_pref.as<uint64_t>(),
-                                       static_cast<int>(m), ctx->sel_hist.as<unsigned long long>(), s));
-        ctx->last_launches = 1;
-    }
-    BMC_CK(ctx, cudaMemcpyAsync(hist, ctx->sel_hist.p, m * 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    BMC_CK(ctx, cudaStreamSynchronize(s));
-    return BMC_OK;
 }
 
 }  // extern "C"

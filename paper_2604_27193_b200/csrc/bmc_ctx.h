@@ -198,6 +198,13 @@ inline int fail(bmc_ctx* ctx, int code, const std::string& msg) {
     return code;
 }
 
+// abi_exception() that also records the message on the context
+inline int abi_exception(bmc_ctx* ctx) {
+    const int rc = abi_exception();
+    if (ctx) ctx->err = get_error();
+    return rc;
+}
+
 #define BMC_CK(ctx, expr)                                                                   \
     do {                                                                                    \
         const cudaError_t e_ = (expr);                                                      \

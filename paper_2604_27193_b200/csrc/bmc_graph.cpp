@@ -280,102 +280,122 @@ extern "C" {
 
 int bmc_cuda_graph_create(bmc_ctx* ctx, size_t n, const bmc_world* world,
                           const bmc_run_opts* opts, bmc_graph** out) {
-    return graph_create(ctx, n, world, opts, nullptr, out);
+    try {
+        return graph_create(ctx, n, world, opts, nullptr, out);
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_graph_create_stats(bmc_ctx* ctx, size_t n, const bmc_world* world,
                                 const bmc_run_opts* opts, const bmc_stats_req* req,
                                 bmc_graph** out) {
-    if (!req) return bmc::fail(ctx, BMC_E_CONFIG, "bmc_cuda_graph_create_stats: null request");
-    return graph_create(ctx, n, world, opts, req, out);
+    try {
+        if (!req) return bmc::fail(ctx, BMC_E_CONFIG, "bmc_cuda_graph_create_stats: null request");
+        return graph_create(ctx, n, world, opts, req, out);
+    } catch (...) {
+        return bmc::abi_exception(ctx);
+    }
 }
 
 int bmc_cuda_graph_stats(bmc_graph* g, bmc_stats* out) {
-    if (!g || !out) return bmc::fail(g ? g->ctx : nullptr, BMC_E_CONFIG, "bmc_cuda_graph_stats: null argument");
-    if (!g->st) return bmc::fail(g->ctx, BMC_E_CONFIG, "bmc_cuda_graph_stats: graph has no statistics stage");
-    if (!g->replayed) return bmc::fail(g->ctx, BMC_E_CONFIG, "bmc_cuda_graph_stats: no decision ran yet");
-    int rc = bmc::prepare(g->ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(g->ctx->mu);
-    const char* dout = g->d_out.as<char>();
-    rc = bmc::stats_compose_mirror(g->st, g->h_stats.as<uint64_t>(), reinterpret_cast<const double*>(dout),
-                                   reinterpret_cast<const uint8_t*>(dout + g->n * 12), g->n, out);
-    if (rc == BMC_OK) out->launches = g->launches;
-    return rc;
+    try {
+        if (!g || !out) return bmc::fail(g ? g->ctx : nullptr, BMC_E_CONFIG, "bmc_cuda_graph_stats: null argument");
+        if (!g->st) return bmc::fail(g->ctx, BMC_E_CONFIG, "bmc_cuda_graph_stats: graph has no statistics stage");
+        if (!g->replayed) return bmc::fail(g->ctx, BMC_E_CONFIG, "bmc_cuda_graph_stats: no decision ran yet");
+        int rc = bmc::prepare(g->ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(g->ctx->mu);
+        const char* dout = g->d_out.as<char>();
+        rc = bmc::stats_compose_mirror(g->st, g->h_stats.as<uint64_t>(), reinterpret_cast<const double*>(dout),
+                                       reinterpret_cast<const uint8_t*>(dout + g->n * 12), g->n, out);
+        if (rc == BMC_OK) out->launches = g->launches;
+        return rc;
+    } catch (...) {
+        return bmc::abi_exception();
+    }
 }
 
 int bmc_cuda_graph_run(bmc_graph* g, const bmc_sample* samples, bmc_result* out,
                        bmc_run_info* info) {
-    if (!g || !samples || !out) return bmc::fail(g ? g->ctx : nullptr, BMC_E_CONFIG, "bmc_cuda_graph_run: null argument");
-    int rc = bmc::prepare(g->ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(g->ctx->mu);
-    const auto t0 = std::chrono::steady_clock::now();
-    const size_t n = g->n;
-    double* h = g->h_terms.as<double>();
-    std::atomic<int> status{BMC_OK};
-    bmc::ctx_pool(g->ctx, g->threads).parallel_for(
-        n,
-        [&](size_t b, size_t e) {
-            const int r = bmc::stage_terms_serial(samples + b, e - b, g->world, h + b, h + n + b,
-                                                  h + 2 * n + b, h + 3 * n + b);
-            if (r != BMC_OK) status = r;
-        },
-        g->threads);
-    if (status != BMC_OK) return bmc::fail(g->ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
-    return replay(g, out, info, t0);
+    try {
+        if (!g || !samples || !out) return bmc::fail(g ? g->ctx : nullptr, BMC_E_CONFIG, "bmc_cuda_graph_run: null argument");
+        int rc = bmc::prepare(g->ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(g->ctx->mu);
+        const auto t0 = std::chrono::steady_clock::now();
+        const size_t n = g->n;
+        double* h = g->h_terms.as<double>();
+        std::atomic<int> status{BMC_OK};
+        bmc::ctx_pool(g->ctx, g->threads).parallel_for(
+            n,
+            [&](size_t b, size_t e) {
+                const int r = bmc::stage_terms_serial(samples + b, e - b, g->world, h + b, h + n + b,
+                                                      h + 2 * n + b, h + 3 * n + b);
+                if (r != BMC_OK) status = r;
+            },
+            g->threads);
+        if (status != BMC_OK) return bmc::fail(g->ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
+        return replay(g, out, info, t0);
+    } catch (...) {
+        return bmc::abi_exception();
+    }
 }
 
 int bmc_cuda_graph_run_model(bmc_graph* g, const bmc_model* model, uint64_t first, bmc_result* out,
                              uint64_t* clamp_count, bmc_run_info* info) {
-    if (!g || !model || !out) return bmc::fail(g ? g->ctx : nullptr, BMC_E_CONFIG, "bmc_cuda_graph_run_model: null argument");
-    int rc = bmc::prepare(g->ctx);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(g->ctx->mu);
-    const auto t0 = std::chrono::steady_clock::now();
-    bmc_run_opts o{};
-    o.sampler = g->sampler;
-    bool dev = false;
-    if ((rc = bmc::use_device_sampler(g->ctx, o, &dev)) != BMC_OK) return rc;
-    if (dev) {
-        if (!g->mexec && (rc = capture_model_graph(g)) != BMC_OK) return rc;
-        bmc::DrawDyn* p = g->h_dyn.as<bmc::DrawDyn>();
-        p->seed = model->seed;
-        p->spec[0] = model->initial_speed;
-        p->spec[1] = model->friction;
-        p->spec[2] = model->grade;
-        p->spec[3] = model->mass;
-        p->spec[4] = model->drag_coeff;
-        p->first = first;
-        if ((rc = replay(g, out, info, t0, true)) != BMC_OK) return rc;
-        const unsigned long long* c = g->h_ctr.as<unsigned long long>();
-        const unsigned flags = static_cast<unsigned>(c[1]);
-        if (flags & bmc::kDrawDomain) {
-            return bmc::fail(g->ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
+    try {
+        if (!g || !model || !out) return bmc::fail(g ? g->ctx : nullptr, BMC_E_CONFIG, "bmc_cuda_graph_run_model: null argument");
+        int rc = bmc::prepare(g->ctx);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(g->ctx->mu);
+        const auto t0 = std::chrono::steady_clock::now();
+        bmc_run_opts o{};
+        o.sampler = g->sampler;
+        bool dev = false;
+        if ((rc = bmc::use_device_sampler(g->ctx, o, &dev)) != BMC_OK) return rc;
+        if (dev) {
+            if (!g->mexec && (rc = capture_model_graph(g)) != BMC_OK) return rc;
+            bmc::DrawDyn* p = g->h_dyn.as<bmc::DrawDyn>();
+            p->seed = model->seed;
+            p->spec[0] = model->initial_speed;
+            p->spec[1] = model->friction;
+            p->spec[2] = model->grade;
+            p->spec[3] = model->mass;
+            p->spec[4] = model->drag_coeff;
+            p->first = first;
+            if ((rc = replay(g, out, info, t0, true)) != BMC_OK) return rc;
+            const unsigned long long* c = g->h_ctr.as<unsigned long long>();
+            const unsigned flags = static_cast<unsigned>(c[1]);
+            if (flags & bmc::kDrawDomain) {
+                return bmc::fail(g->ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
+            }
+            if (flags & bmc::kDrawUnported) {
+                return bmc::fail(g->ctx, BMC_E_RANGE, "device sampler: a libm argument left the ported glibc range");
+            }
+            if (clamp_count) *clamp_count = c[0];
+            return BMC_OK;
         }
-        if (flags & bmc::kDrawUnported) {
-            return bmc::fail(g->ctx, BMC_E_RANGE, "device sampler: a libm argument left the ported glibc range");
-        }
-        if (clamp_count) *clamp_count = c[0];
-        return BMC_OK;
+        const size_t n = g->n;
+        double* h = g->h_terms.as<double>();
+        std::atomic<int> status{BMC_OK};
+        std::atomic<uint64_t> clamps{0};
+        bmc::ctx_pool(g->ctx, g->threads).parallel_for(
+            n,
+            [&](size_t b, size_t e) {
+                uint64_t c = 0;
+                const int r = bmc::draw_terms_serial(*model, first + b, e - b, g->world, h + b, h + n + b,
+                                                     h + 2 * n + b, h + 3 * n + b, &c);
+                clamps += c;
+                if (r != BMC_OK) status = r;
+            },
+            g->threads);
+        if (status != BMC_OK) return bmc::fail(g->ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
+        if (clamp_count) *clamp_count = clamps.load();
+        return replay(g, out, info, t0);
+    } catch (...) {
+        return bmc::abi_exception();
     }
-    const size_t n = g->n;
-    double* h = g->h_terms.as<double>();
-    std::atomic<int> status{BMC_OK};
-    std::atomic<uint64_t> clamps{0};
-    bmc::ctx_pool(g->ctx, g->threads).parallel_for(
-        n,
-        [&](size_t b, size_t e) {
-            uint64_t c = 0;
-            const int r = bmc::draw_terms_serial(*model, first + b, e - b, g->world, h + b, h + n + b,
-                                                 h + 2 * n + b, h + 3 * n + b, &c);
-            clamps += c;
-            if (r != BMC_OK) status = r;
-        },
-        g->threads);
-    if (status != BMC_OK) return bmc::fail(g->ctx, BMC_E_DOMAIN, "friction_limit: weight-transfer denominator <= 0");
-    if (clamp_count) *clamp_count = clamps.load();
-    return replay(g, out, info, t0);
 }
 
 void bmc_cuda_graph_destroy(bmc_graph* g) {

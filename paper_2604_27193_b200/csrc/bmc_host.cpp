@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <new>
+#include <stdexcept>
 #include <string>
 
 namespace bmc {
@@ -24,6 +26,21 @@ thread_local std::string t_error;
 }
 
 void set_error(const std::string& msg) { t_error = msg; }
+
+int abi_exception() {
+    try {
+        throw;
+    } catch (const std::bad_alloc&) {
+        set_error("out of host memory");
+        return BMC_E_NOMEM;
+    } catch (const std::exception& e) {
+        set_error(std::string("internal error: ") + e.what());
+        return BMC_E_CONFIG;
+    } catch (...) {
+        set_error("internal error: unknown exception");
+        return BMC_E_CONFIG;
+    }
+}
 const std::string& get_error() { return t_error; }
 
 // ----------------------------------------------------------------- world
@@ -275,46 +292,54 @@ ThreadPool& host_pool() {
 
 extern "C" int bmc_draw_range(const bmc_model* model, uint64_t first, size_t n, bmc_sample* out,
                               uint64_t* clamp_count, int threads) {
-    if (model == nullptr || out == nullptr) {
-        bmc::set_error("bmc_draw_range: null argument");
-        return BMC_E_CONFIG;
+    try {
+        if (model == nullptr || out == nullptr) {
+            bmc::set_error("bmc_draw_range: null argument");
+            return BMC_E_CONFIG;
+        }
+        if (n == 0) {
+            bmc::set_error("samples: must be >= 1");  // sampling.cpp:68-70
+            return BMC_E_CONFIG;
+        }
+        std::atomic<uint64_t> clamps{0};
+        bmc::host_pool().parallel_for(
+            n,
+            [&](std::size_t b, std::size_t e) {
+                clamps += bmc::draw_range_serial(*model, first + b, e - b, out + b);
+            },
+            bmc::resolve_threads(threads));
+        if (clamp_count) *clamp_count = clamps.load();
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception();
     }
-    if (n == 0) {
-        bmc::set_error("samples: must be >= 1");  // sampling.cpp:68-70
-        return BMC_E_CONFIG;
-    }
-    std::atomic<uint64_t> clamps{0};
-    bmc::host_pool().parallel_for(
-        n,
-        [&](std::size_t b, std::size_t e) {
-            clamps += bmc::draw_range_serial(*model, first + b, e - b, out + b);
-        },
-        bmc::resolve_threads(threads));
-    if (clamp_count) *clamp_count = clamps.load();
-    return BMC_OK;
 }
 
 extern "C" int bmc_stage_terms(const bmc_sample* samples, size_t n, const bmc_world* world,
                                double* v0, double* floor, double* drag, double* grade,
                                int threads) {
-    if (samples == nullptr || world == nullptr || !v0 || !floor || !drag || !grade) {
-        bmc::set_error("bmc_stage_terms: null argument");
-        return BMC_E_CONFIG;
+    try {
+        if (samples == nullptr || world == nullptr || !v0 || !floor || !drag || !grade) {
+            bmc::set_error("bmc_stage_terms: null argument");
+            return BMC_E_CONFIG;
+        }
+        std::atomic<int> status{BMC_OK};
+        bmc::host_pool().parallel_for(
+            n,
+            [&](std::size_t b, std::size_t e) {
+                const int rc = bmc::stage_terms_serial(samples + b, e - b, *world, v0 + b,
+                                                       floor + b, drag + b, grade + b);
+                if (rc != BMC_OK) status = rc;
+            },
+            bmc::resolve_threads(threads));
+        if (status != BMC_OK) {
+            bmc::set_error("friction_limit: weight-transfer denominator <= 0");
+            return status;
+        }
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception();
     }
-    std::atomic<int> status{BMC_OK};
-    bmc::host_pool().parallel_for(
-        n,
-        [&](std::size_t b, std::size_t e) {
-            const int rc = bmc::stage_terms_serial(samples + b, e - b, *world, v0 + b,
-                                                   floor + b, drag + b, grade + b);
-            if (rc != BMC_OK) status = rc;
-        },
-        bmc::resolve_threads(threads));
-    if (status != BMC_OK) {
-        bmc::set_error("friction_limit: weight-transfer denominator <= 0");
-        return status;
-    }
-    return BMC_OK;
 }
 
 // ------------------------------------------------------------ results.csv
@@ -324,50 +349,54 @@ extern "C" int bmc_stage_terms(const bmc_sample* samples, size_t n, const bmc_wo
 // by the host pool in slices and written in index order.
 extern "C" int bmc_write_results_csv(const char* path, const bmc_result* r, size_t n,
                                      int threads) {
-    if (!path || (n && !r)) {
-        bmc::set_error("bmc_write_results_csv: null argument");
-        return BMC_E_CONFIG;
-    }
-    std::FILE* f = std::fopen(path, "wb");
-    if (!f) {
-        bmc::set_error(std::string("cannot open for writing: ") + path);  // IoError analogue
-        return BMC_E_IO;
-    }
-    const char* header = "index,d_stop_m,t_stop_s,horizon_flag\n";
-    bool ok = std::fputs(header, f) >= 0;
-    const std::size_t kSlice = std::size_t{1} << 18;
-    std::vector<std::string> bufs;
-    for (std::size_t s0 = 0; ok && s0 < n; s0 += kSlice * 64) {
-        const std::size_t s1 = std::min(n, s0 + kSlice * 64);
-        const std::size_t parts = (s1 - s0 + kSlice - 1) / kSlice;
-        bufs.assign(parts, std::string());
-        bmc::host_pool().parallel_for(
-            parts,
-            [&](std::size_t b, std::size_t e) {
-                char line[128];
-                for (std::size_t p = b; p < e; ++p) {
-                    std::string& out = bufs[p];
-                    const std::size_t i0 = s0 + p * kSlice, i1 = std::min(s1, i0 + kSlice);
-                    out.reserve((i1 - i0) * 48);
-                    for (std::size_t i = i0; i < i1; ++i) {
-                        const int len = std::snprintf(line, sizeof line, "%zu,%.17g,%.17g,%c\n", i,
-                                                      r[i].stop_distance, r[i].stop_time,
-                                                      r[i].hit_horizon ? '1' : '0');
-                        out.append(line, static_cast<std::size_t>(len));
-                    }
-                }
-            },
-            bmc::resolve_threads(threads));
-        for (const auto& b : bufs) {
-            if (std::fwrite(b.data(), 1, b.size(), f) != b.size()) ok = false;
+    try {
+        if (!path || (n && !r)) {
+            bmc::set_error("bmc_write_results_csv: null argument");
+            return BMC_E_CONFIG;
         }
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) {
+            bmc::set_error(std::string("cannot open for writing: ") + path);  // IoError analogue
+            return BMC_E_IO;
+        }
+        const char* header = "index,d_stop_m,t_stop_s,horizon_flag\n";
+        bool ok = std::fputs(header, f) >= 0;
+        const std::size_t kSlice = std::size_t{1} << 18;
+        std::vector<std::string> bufs;
+        for (std::size_t s0 = 0; ok && s0 < n; s0 += kSlice * 64) {
+            const std::size_t s1 = std::min(n, s0 + kSlice * 64);
+            const std::size_t parts = (s1 - s0 + kSlice - 1) / kSlice;
+            bufs.assign(parts, std::string());
+            bmc::host_pool().parallel_for(
+                parts,
+                [&](std::size_t b, std::size_t e) {
+                    char line[128];
+                    for (std::size_t p = b; p < e; ++p) {
+                        std::string& out = bufs[p];
+                        const std::size_t i0 = s0 + p * kSlice, i1 = std::min(s1, i0 + kSlice);
+                        out.reserve((i1 - i0) * 48);
+                        for (std::size_t i = i0; i < i1; ++i) {
+                            const int len = std::snprintf(line, sizeof line, "%zu,%.17g,%.17g,%c\n", i,
+                                                          r[i].stop_distance, r[i].stop_time,
+                                                          r[i].hit_horizon ? '1' : '0');
+                            out.append(line, static_cast<std::size_t>(len));
+                        }
+                    }
+                },
+                bmc::resolve_threads(threads));
+            for (const auto& b : bufs) {
+                if (std::fwrite(b.data(), 1, b.size(), f) != b.size()) ok = false;
+            }
+        }
+        if (std::fclose(f) != 0) ok = false;
+        if (!ok) {
+            bmc::set_error(std::string("write failed: ") + path);
+            return BMC_E_IO;
+        }
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception();
     }
-    if (std::fclose(f) != 0) ok = false;
-    if (!ok) {
-        bmc::set_error(std::string("write failed: ") + path);
-        return BMC_E_IO;
-    }
-    return BMC_OK;
 }
 
 // parse_results_csv (io.cpp:94-123) + the step reconstruction of cmd_verify
@@ -375,59 +404,63 @@ extern "C" int bmc_write_results_csv(const char* path, const bmc_result* r, size
 // BMC_E_RANGE if it exceeds cap (then *n_out is the count needed).
 extern "C" int bmc_read_results_csv(const char* path, double dt, bmc_result* out, size_t cap,
                                     size_t* n_out) {
-    if (!path || !n_out) {
-        bmc::set_error("bmc_read_results_csv: null argument");
-        return BMC_E_CONFIG;
-    }
-    std::FILE* f = std::fopen(path, "rb");
-    if (!f) {
-        bmc::set_error(std::string("cannot open for reading: ") + path);
-        return BMC_E_IO;
-    }
-    char line[512];
-    if (!std::fgets(line, sizeof line, f) ||
-        std::strcmp(line, "index,d_stop_m,t_stop_s,horizon_flag\n") != 0) {
+    try {
+        if (!path || !n_out) {
+            bmc::set_error("bmc_read_results_csv: null argument");
+            return BMC_E_CONFIG;
+        }
+        std::FILE* f = std::fopen(path, "rb");
+        if (!f) {
+            bmc::set_error(std::string("cannot open for reading: ") + path);
+            return BMC_E_IO;
+        }
+        char line[512];
+        if (!std::fgets(line, sizeof line, f) ||
+            std::strcmp(line, "index,d_stop_m,t_stop_s,horizon_flag\n") != 0) {
+            std::fclose(f);
+            bmc::set_error("results csv: missing or unexpected header");
+            return BMC_E_IO;
+        }
+        std::size_t count = 0, line_no = 1;
+        int rc = BMC_OK;
+        while (std::fgets(line, sizeof line, f)) {
+            ++line_no;
+            if (line[0] == '\n' || line[0] == '\0') continue;
+            unsigned long long index = 0;
+            unsigned flag = 0;
+            double d = 0.0, t = 0.0;
+            if (std::sscanf(line, "%llu,%lf,%lf,%u", &index, &d, &t, &flag) != 4) {
+                bmc::set_error("results csv: malformed line " + std::to_string(line_no));
+                rc = BMC_E_IO;
+                break;
+            }
+            if (index != count) {
+                bmc::set_error("results csv: non-contiguous index at line " + std::to_string(line_no));
+                rc = BMC_E_IO;
+                break;
+            }
+            if (out && count < cap) {
+                bmc_result r;
+                std::memset(&r, 0, sizeof r);
+                r.stop_distance = d;
+                r.stop_time = t;
+                r.steps = std::llround(t / dt);
+                r.hit_horizon = flag != 0 ? 1 : 0;
+                out[count] = r;
+            }
+            ++count;
+        }
         std::fclose(f);
-        bmc::set_error("results csv: missing or unexpected header");
-        return BMC_E_IO;
-    }
-    std::size_t count = 0, line_no = 1;
-    int rc = BMC_OK;
-    while (std::fgets(line, sizeof line, f)) {
-        ++line_no;
-        if (line[0] == '\n' || line[0] == '\0') continue;
-        unsigned long long index = 0;
-        unsigned flag = 0;
-        double d = 0.0, t = 0.0;
-        if (std::sscanf(line, "%llu,%lf,%lf,%u", &index, &d, &t, &flag) != 4) {
-            bmc::set_error("results csv: malformed line " + std::to_string(line_no));
-            rc = BMC_E_IO;
-            break;
+        *n_out = count;
+        if (rc != BMC_OK) return rc;
+        if (count > cap) {
+            bmc::set_error("results csv: output buffer too small");
+            return BMC_E_RANGE;
         }
-        if (index != count) {
-            bmc::set_error("results csv: non-contiguous index at line " + std::to_string(line_no));
-            rc = BMC_E_IO;
-            break;
-        }
-        if (out && count < cap) {
-            bmc_result r;
-            std::memset(&r, 0, sizeof r);
-            r.stop_distance = d;
-            r.stop_time = t;
-            r.steps = std::llround(t / dt);
-            r.hit_horizon = flag != 0 ? 1 : 0;
-            out[count] = r;
-        }
-        ++count;
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception();
     }
-    std::fclose(f);
-    *n_out = count;
-    if (rc != BMC_OK) return rc;
-    if (count > cap) {
-        bmc::set_error("results csv: output buffer too small");
-        return BMC_E_RANGE;
-    }
-    return BMC_OK;
 }
 
 extern "C" const char* bmc_last_error(void) { return bmc::get_error().c_str(); }

@@ -80,6 +80,10 @@ int draw_terms_serial(const bmc_model& m, uint64_t first, std::size_t n, const b
                       double* v0, double* floor, double* drag, double* grade, uint64_t* clamps);
 
 void set_error(const std::string& msg);
+// Called from the catch (...) around every C-ABI entry point: the in-flight
+// C++ exception becomes an error code + message (no exception crosses the
+// ABI).  std::bad_alloc -> BMC_E_NOMEM, anything else -> BMC_E_CONFIG.
+int abi_exception();
 const std::string& get_error();
 
 } // namespace bmc

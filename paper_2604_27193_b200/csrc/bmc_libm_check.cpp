@@ -125,27 +125,35 @@ bool device_sampler_supported(std::string* why) {
 }  // namespace bmc
 
 extern "C" int bmc_libm_selftest(uint64_t n, uint64_t seed, int threads, uint64_t* mismatches) {
-    if (mismatches == nullptr) {
-        bmc::set_error("bmc_libm_selftest: null argument");
-        return BMC_E_CONFIG;
-    }
-    bmc::libm_port_check(n, seed, bmc::resolve_threads(threads), mismatches);
-    for (int k = 0; k < 7; ++k) {
-        if (mismatches[k]) {
-            bmc::set_error("glibc port differs from the host libm");
+    try {
+        if (mismatches == nullptr) {
+            bmc::set_error("bmc_libm_selftest: null argument");
             return BMC_E_CONFIG;
         }
+        bmc::libm_port_check(n, seed, bmc::resolve_threads(threads), mismatches);
+        for (int k = 0; k < 7; ++k) {
+            if (mismatches[k]) {
+                bmc::set_error("glibc port differs from the host libm");
+                return BMC_E_CONFIG;
+            }
+        }
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception();
     }
-    return BMC_OK;
 }
 
 extern "C" int bmc_device_sampler_available(int* available) {
-    if (available == nullptr) {
-        bmc::set_error("bmc_device_sampler_available: null argument");
-        return BMC_E_CONFIG;
+    try {
+        if (available == nullptr) {
+            bmc::set_error("bmc_device_sampler_available: null argument");
+            return BMC_E_CONFIG;
+        }
+        std::string why;
+        *available = bmc::device_sampler_supported(&why) ? 1 : 0;
+        if (!*available) bmc::set_error(why);
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception();
     }
-    std::string why;
-    *available = bmc::device_sampler_supported(&why) ? 1 : 0;
-    if (!*available) bmc::set_error(why);
-    return BMC_OK;
 }

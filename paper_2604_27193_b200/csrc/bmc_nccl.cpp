@@ -102,33 +102,41 @@ using bmc::fail;
 extern "C" {
 
 int bmc_nccl_available(int* version) {
-    const bmc::NcclApi& a = bmc::api();
-    if (version) *version = a.version;
-    if (!a.ok) return fail(nullptr, BMC_E_CUDA, a.why);
-    return BMC_OK;
+    try {
+        const bmc::NcclApi& a = bmc::api();
+        if (version) *version = a.version;
+        if (!a.ok) return fail(nullptr, BMC_E_CUDA, a.why);
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception();
+    }
 }
 
 int bmc_nccl_init_all(int ndev, const int* devices, bmc_comm** comms) {
-    if (ndev < 1 || !devices || !comms) return fail(nullptr, BMC_E_CONFIG, "bmc_nccl_init_all: bad arguments");
-    const bmc::NcclApi& a = bmc::api();
-    if (!a.ok) return fail(nullptr, BMC_E_CUDA, a.why);
-    std::vector<ncclComm_t> c(static_cast<size_t>(ndev), nullptr);
-    const ncclResult_t e = a.CommInitAll(c.data(), ndev, devices);
-    if (e != ncclSuccess) return fail(nullptr, BMC_E_CUDA, std::string("ncclCommInitAll: ") + a.GetErrorString(e));
-    for (int r = 0; r < ndev; ++r) {
-        auto* x = new bmc_comm;
-        x->comm = c[static_cast<size_t>(r)];
-        x->device = devices[r];
-        x->rank = r;
-        x->world = ndev;
-        x->merge.user = x;
-        x->merge.world = ndev;
-        x->merge.rank = r;
-        x->merge.allreduce_u64 = bmc::nccl_allreduce;
-        x->merge.allgather_u64 = bmc::nccl_allgather;
-        comms[r] = x;
+    try {
+        if (ndev < 1 || !devices || !comms) return fail(nullptr, BMC_E_CONFIG, "bmc_nccl_init_all: bad arguments");
+        const bmc::NcclApi& a = bmc::api();
+        if (!a.ok) return fail(nullptr, BMC_E_CUDA, a.why);
+        std::vector<ncclComm_t> c(static_cast<size_t>(ndev), nullptr);
+        const ncclResult_t e = a.CommInitAll(c.data(), ndev, devices);
+        if (e != ncclSuccess) return fail(nullptr, BMC_E_CUDA, std::string("ncclCommInitAll: ") + a.GetErrorString(e));
+        for (int r = 0; r < ndev; ++r) {
+            auto* x = new bmc_comm;
+            x->comm = c[static_cast<size_t>(r)];
+            x->device = devices[r];
+            x->rank = r;
+            x->world = ndev;
+            x->merge.user = x;
+            x->merge.world = ndev;
+            x->merge.rank = r;
+            x->merge.allreduce_u64 = bmc::nccl_allreduce;
+            x->merge.allgather_u64 = bmc::nccl_allgather;
+            comms[r] = x;
+        }
+        return BMC_OK;
+    } catch (...) {
+        return bmc::abi_exception();
     }
-    return BMC_OK;
 }
 
 const bmc_merge* bmc_nccl_merge(const bmc_comm* comm) { return comm ? &comm->merge : nullptr; }
