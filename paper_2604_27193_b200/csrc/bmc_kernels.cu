@@ -815,37 +815,17 @@ __global__ void __launch_bounds__(256, BMC_SCATTER_PRELOAD ? 2 : 1)
     }
 }
 
-#ifndef BMC_UNPERMUTE_ILP
-#define BMC_UNPERMUTE_ILP 4
-#endif
-// Index-order gather of the packed sorted outputs: kUnp independent
-// (slot -> record) gathers in flight per thread, one 16-B load each; the
-// records sit at random slots, so each costs a full 32-B sector (73 B/sample
-// DRAM for 33 algorithmic).  8 in flight: 2.47 ms but 123 B/sample of DRAM
-// reads; 4: 2.66 ms at 73 B/sample (ncu, profiles/round2_hbm_stage_ab.txt).
+// Index-order gather of the packed sorted outputs.  The 16-B records sit at
+// random slots, so each costs a full 32-B sector (73 B/sample DRAM for 33
+// algorithmic).  Measured and not adopted (ncu, profiles/round2_hbm_stage_ab.txt
+// section F): 4 or 8 gathers in flight per thread with one 16-B streaming
+// load each -- 2.68 / 2.47 ms against 2.66 ms, but 123 B/sample of DRAM reads.
 __global__ void __launch_bounds__(256) unpermute_kernel(const PackedOut* packed_out,
                                                         const uint32_t* inv_perm, uint64_t n,
                                                         double* d, int32_t* steps, uint8_t* hz) {
-    constexpr int kUnp = BMC_UNPERMUTE_ILP;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    for (; j + (kUnp - 1) * stride < n; j += kUnp * stride) {
-        uint32_t slot[kUnp];
-        double2 r[kUnp];  // one 16-B load per record: {x, (steps, hit_horizon)}
-#pragma unroll
-        for (int k = 0; k < kUnp; ++k) slot[k] = __ldcs(inv_perm + j + k * stride);
-#pragma unroll
-        for (int k = 0; k < kUnp; ++k) r[k] = __ldcs(reinterpret_cast<const double2*>(packed_out) + slot[k]);
-#pragma unroll
-        for (int k = 0; k < kUnp; ++k) {
-            const uint64_t q = j + k * stride;
-            const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r[k].y));
-            if (d) d[q] = r[k].x;
-            if (steps) steps[q] = static_cast<int32_t>(static_cast<uint32_t>(w));
-            if (hz) hz[q] = static_cast<uint8_t>(w >> 32);
-        }
-    }
-    for (; j < n; j += stride) {
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+         j += stride) {
         const PackedOut r = packed_out[inv_perm[j]];
         if (d) d[j] = r.x;
         if (steps) steps[j] = r.steps;
