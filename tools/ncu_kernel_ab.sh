@@ -1,3 +1,4 @@
+#!/bin/bash
 # usage: bash tools/_ab.sh "regex" variant...   (ncu kernel times, in-tree first)
 mkdir -p gpurun_out
 re=$1; shift
