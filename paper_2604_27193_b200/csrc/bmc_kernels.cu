@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictArgs P) {
 
 __global__ void __launch_bounds__(1024) bin_scan_kernel(unsigned int* hist_all, int buckets) {
     // exclusive scan, in place: counts -> start cursor of each bucket; block
-    // w scans window w, whose sorted slots start at w * 2^20 (full windows)
+    // w scans window w, whose sorted slots start at w * 2^kBinWindowLog2 (full windows)
     unsigned int* hist = hist_all + static_cast<size_t>(blockIdx.x) * buckets;
     const unsigned int base = static_cast<unsigned int>(blockIdx.x) << kBinWindowLog2;
     using Scan = cub::BlockScan<unsigned int, 1024>;
@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(256, BMC_SCATTER_PRELOAD ? 2 : 1)
             if (i < n) rank[k] = atomicAdd(&s_cnt[key[k]], 1u);
         }
         __syncthreads();
-        // a tile lies inside one binning window (2^20 is a multiple of kTile)
+        // a tile lies inside one binning window (2^kBinWindowLog2 is a multiple of kTile)
         unsigned int* wcur = cursor + (tile >> kBinWindowLog2) * static_cast<uint64_t>(buckets);
         for (int b = threadIdx.x; b < kMaxBuckets; b += 256) {
             const unsigned c = s_cnt[b];
