@@ -403,13 +403,14 @@ int trace_level() {
 // h2d stream copies them, the compute stream bins + rolls out, and either
 // the d2h stream returns the compact outputs for the host unpack, or the
 // kernel writes straight into caller-owned device outputs.
-// Why three: the persistent rollout of chunk k+1 takes every SM during the
-// tail of chunk k's rollout, so chunk k's unpermute (and with it its D2H)
-// only runs after chunk k+1's rollout.  With two slots the host, which must
-// unpack chunk k before staging chunk k+2 into the same slot, then left the
-// device idle ~9.5 ms every second chunk (BMC_PIPE_TRACE=2 timeline,
-// profiles/round2_summary.md); a third slot gives the host a whole chunk of
-// slack.
+// The persistent rollout of chunk k+1 takes every SM during the tail of
+// chunk k's rollout, so any kernel after chunk k's rollout (an unpermute)
+// waited for the whole of chunk k+1, its D2H and host unpack came late, and
+// with two slots the host -- which unpacks chunk k before staging chunk k+2
+// into the same slot -- left the device idle ~9.5 ms every second chunk
+// (BMC_PIPE_TRACE=2 timeline, profiles/round2_pipeline_trace.txt).  Chunks
+// therefore write their outputs directly (direct_outputs_for), and a third
+// slot gives the host a whole chunk of slack: 1040 -> 940 ms at 1e8.
 int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const bmc_run_opts& o,
                  uint64_t n, const bmc_sample* samples, const bmc_model* model, uint64_t first,
                  bmc_result* host_out, const bmc_outputs* dev_out, bmc_run_info* info,
