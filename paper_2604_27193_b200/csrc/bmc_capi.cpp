@@ -432,7 +432,27 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
         const char* e = std::getenv("BMC_PIPE_SLOTS");
         return (e && e[0] == '2') ? uint64_t{2} : uint64_t{sizeof(bmc_ctx::slots) / sizeof(Slot)};
     }();
-    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    // Chunk schedule: fixed chunks; long automatic schedules (>= 8 chunks)
+    // start with a chunk/4 piece so less host staging and H2D is exposed
+    // before the device starts: 1e8 host -> host 932.0 -> 929.3 ms (3 slots,
+    // profiles/round2_pipeline_trace.txt; BMC_PIPE_HEAD=d sets the divisor,
+    // 1 = off).  Ramping both edges down lost 7 ms with two slots.
+    static const uint64_t head_div = [] {
+        const char* e = std::getenv("BMC_PIPE_HEAD");
+        const long v = e ? std::atol(e) : 4;
+        return static_cast<uint64_t>(v >= 1 && v <= 64 ? v : 4);
+    }();
+    std::vector<std::pair<uint64_t, uint64_t>> sched;
+    {
+        uint64_t off = 0;
+        if (head_div > 1 && o.chunk_samples == 0 && n >= 8 * chunk) {
+            const uint64_t h = std::max<uint64_t>(1, chunk / head_div);
+            sched.emplace_back(0, h);
+            off = h;
+        }
+        for (; off < n; off += chunk) sched.emplace_back(off, std::min(chunk, n - off));
+    }
+    const uint64_t nchunks = sched.size();
     const uint64_t used_slots = std::min(kSlots, nchunks);
     const int direct = direct_outputs_for(chunk);
     for (uint64_t q = 0; q < used_slots; ++q) {
@@ -521,12 +541,6 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
         return BMC_OK;
     };
 
-    // Chunk schedule: fixed chunks.  (Smaller edge chunks to shorten the
-    // exposed first staging / last unpack were measured at 1e8: a symmetric
-    // chunk/8 ramp lost 7 ms per call, a chunk/4 first chunk won 2.6 ms
-    // (0.27%, within run-to-run spread); profiles/round2_summary.md.)
-    std::vector<std::pair<uint64_t, uint64_t>> sched;
-    for (uint64_t off = 0; off < n; off += chunk) sched.emplace_back(off, std::min(chunk, n - off));
     for (uint64_t k = 0; k < nchunks; ++k) {
         Slot& s = ctx->slots[k % kSlots];
         if ((rc = finish(s)) != BMC_OK) return rc;
