@@ -451,7 +451,6 @@ int run_pipeline(bmc_ctx* ctx, const bmc_world& w, const WorldDerived& d, const 
             off = h;
         }
         for (; off < n; off += chunk) sched.emplace_back(off, std::min(chunk, n - off));
-        }
     }
     const uint64_t nchunks = sched.size();
     const uint64_t used_slots = std::min(kSlots, nchunks);
