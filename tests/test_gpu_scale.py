@@ -170,3 +170,29 @@ def test_host_pipeline_above_8m_bitwise(ref, executor):
     assert np.array_equal(got["stop_distance"].view(np.uint64), want["stop_distance"].view(np.uint64))
     assert np.array_equal(got["steps"], want["steps"])
     assert np.array_equal(got["stop_time"].view(np.uint64), want["stop_time"].view(np.uint64))
+
+
+def test_streamed_model_head_chunk_schedule(ref, executor):
+    """bmc_cuda_run_model with the automatic schedule at >= 8 chunks: a
+    chunk/4 first piece, then 4M-sample chunks over three slot streams with
+    direct chunk outputs.  Windows across every chunk boundary equal the
+    reference, and the whole output equals an explicit fixed-chunk run."""
+    n = 8 * (1 << 22) + 12345
+    model = _to_model(Model(seed=6))
+    rep, _ = executor.run_model(model, n)
+    head = (1 << 22) // 4
+    assert rep.chunks == 1 + (n - head + (1 << 22) - 1) // (1 << 22)
+    got = rep.results
+    w = 4_000
+    bounds = [head] + [head + k * (1 << 22) for k in range(1, rep.chunks - 1)]
+    for b in [0] + bounds + [n - w // 2]:
+        first = max(0, min(n - w, b - w // 2))
+        smp, _ = bmc.draw_batch(model, w, first=first)
+        want, _, _ = ref.run(smp, World(), "parallel")
+        g = got[first:first + w]
+        assert np.array_equal(g["stop_distance"].view(np.uint64),
+                              want["stop_distance"].view(np.uint64)), first
+        assert np.array_equal(g["steps"], want["steps"]), first
+    fixed, _ = executor.run_model(model, n, chunk=1 << 22)
+    assert fixed.chunks == (n + (1 << 22) - 1) // (1 << 22)
+    assert np.array_equal(fixed.results.view(np.uint8), got.view(np.uint8))
